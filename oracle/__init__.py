@@ -1,0 +1,180 @@
+"""CPU oracle for the chaotic-iteration PRNG hot path (arXiv 1112.5239).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_1112_5239_b200`` never imports it and
+shares no code with it.
+
+The arithmetic lives in ``ciprng_oracle.c`` (plain single-threaded C99, each
+function citing the PAPER.md passage it follows).  This module is ctypes
+marshalling only, plus numpy views of the oracle's per-stream structs.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ciprng_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+V0, V1, V2 = 0, 1, 2
+# words (u32) per stream in the oracle's own structs (see ciprng_oracle.c)
+STATE_WORDS = {V0: 24, V1: 6, V2: 18}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain -O2, no vectorisation flags)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", _SRC, "-o", _LIB]
+        )
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        u64, u32, i32, vp = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int, ctypes.c_void_p
+        L.orc_xor_step.argtypes, L.orc_xor_step.restype = [u64, u64], u64
+        L.orc_xorshift32.argtypes, L.orc_xorshift32.restype = [vp], u32
+        L.orc_xor64.argtypes, L.orc_xor64.restype = [vp], u64
+        L.orc_xor128_64.argtypes, L.orc_xor128_64.restype = [vp], u64
+        L.orc_xorwow_64.argtypes, L.orc_xorwow_64.restype = [vp, vp], u64
+        L.orc_xor128_32.argtypes, L.orc_xor128_32.restype = [vp], u32
+        L.orc_mix64.argtypes, L.orc_mix64.restype = [u64], u64
+        L.orc_splitmix_word.argtypes, L.orc_splitmix_word.restype = [u64, u64, u32], u64
+        L.orc_moduli.argtypes, L.orc_moduli.restype = [vp, i32], i32
+        L.orc_bbs_step.argtypes, L.orc_bbs_step.restype = [u32, u32], u32
+        L.orc_state_size.argtypes, L.orc_state_size.restype = [i32], ctypes.c_size_t
+        L.orc_grid_init.argtypes, L.orc_grid_init.restype = [i32, u64, u64, u64, i32, vp], i32
+        L.orc_grid_generate.argtypes = [i32, vp, u64, u32, vp, u64, vp]
+        L.orc_grid_generate.restype = i32
+        L.orc_stats_words.argtypes, L.orc_stats_words.restype = [vp, u64, u64, vp], i32
+        L.orc_digest_words.argtypes, L.orc_digest_words.restype = [vp, u64, u64, u64], u64
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+# --------------------------------------------------------------------------
+# scalar primitives
+# --------------------------------------------------------------------------
+def xor_step(x: int, s: int) -> int:
+    return lib().orc_xor_step(x, s)
+
+
+def xorshift32_seq(z: int, k: int) -> list[int]:
+    st = np.array([z], dtype=np.uint32)
+    return [lib().orc_xorshift32(_ptr(st)) for _ in range(k)]
+
+
+def xor64_seq(a: int, k: int) -> list[int]:
+    st = np.array([a], dtype=np.uint64)
+    return [lib().orc_xor64(_ptr(st)) for _ in range(k)]
+
+
+def xor128_64_seq(b, k: int) -> list[int]:
+    st = np.array(b, dtype=np.uint64)
+    return [lib().orc_xor128_64(_ptr(st)) for _ in range(k)]
+
+
+def xorwow_64_seq(c, d: int, k: int) -> list[int]:
+    st = np.array(c, dtype=np.uint64)
+    dd = np.array([d], dtype=np.uint64)
+    return [lib().orc_xorwow_64(_ptr(st), _ptr(dd)) for _ in range(k)]
+
+
+def xor128_32_seq(b, k: int) -> list[int]:
+    st = np.array(b, dtype=np.uint32)
+    return [lib().orc_xor128_32(_ptr(st)) for _ in range(k)]
+
+
+def mix64(z: int) -> int:
+    return lib().orc_mix64(z)
+
+
+def splitmix_word(seed: int, s: int, k: int) -> int:
+    return lib().orc_splitmix_word(seed, s, k)
+
+
+def moduli() -> list[int]:
+    buf = np.zeros(256, dtype=np.uint32)
+    n = lib().orc_moduli(_ptr(buf), 256)
+    return [int(v) for v in buf[:n]]
+
+
+def bbs_step(y: int, M: int) -> int:
+    return lib().orc_bbs_step(y, M)
+
+
+# --------------------------------------------------------------------------
+# grid level
+# --------------------------------------------------------------------------
+class OracleError(RuntimeError):
+    pass
+
+
+def init_states(variant: int, seed: int, first_stream: int, n_local: int,
+                paper_defaults: bool = False) -> np.ndarray:
+    """Per-stream states as a (n_local, STATE_WORDS[variant]) uint32 array."""
+    st = np.zeros((n_local, STATE_WORDS[variant]), dtype=np.uint32)
+    rc = lib().orc_grid_init(variant, seed & (2**64 - 1), first_stream, n_local,
+                             int(paper_defaults), _ptr(st))
+    if rc != 0:
+        raise OracleError(f"orc_grid_init rc={rc}")
+    return st
+
+
+def generate(variant: int, states: np.ndarray, n: int, comb_size: int = 32,
+             comb: np.ndarray | None = None) -> np.ndarray:
+    """Advance `states` in place by one call of n rounds; returns (n_local, n) uint32."""
+    assert states.dtype == np.uint32 and states.flags.c_contiguous
+    n_local = states.shape[0]
+    out = np.zeros((n_local, n), dtype=np.uint32)
+    cb = None if comb is None else np.ascontiguousarray(comb, dtype=np.uint8)
+    rc = lib().orc_grid_generate(variant, _ptr(states), n_local, comb_size, _ptr(cb), n, _ptr(out))
+    if rc != 0:
+        raise OracleError(f"orc_grid_generate rc={rc}")
+    return out
+
+
+def stats(words: np.ndarray, acc: np.ndarray | None = None) -> np.ndarray:
+    """258 u64 consumer statistics of a (n_local, n) block of one call."""
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    acc = np.zeros(258, dtype=np.uint64) if acc is None else acc
+    rc = lib().orc_stats_words(_ptr(words), words.shape[0], words.shape[1], _ptr(acc))
+    if rc != 0:
+        raise OracleError(f"orc_stats_words rc={rc}")
+    return acc
+
+
+def digest(words: np.ndarray, first_stream: int = 0) -> int:
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    return lib().orc_digest_words(_ptr(words), first_stream, words.shape[0], words.shape[1])
+
+
+def state_planes(variant: int, states: np.ndarray) -> np.ndarray:
+    """The oracle's per-stream structs viewed as the C-ABI's SoA u32 planes
+    (include/ciprng.h, "State layout"): plane k holds word k of every stream.
+    V0 drops the struct's trailing pad word."""
+    nplanes = {V0: 23, V1: 6, V2: 18}[variant]
+    return np.ascontiguousarray(states[:, :nplanes].T)
+
+
+def states_from_planes(variant: int, planes: np.ndarray) -> np.ndarray:
+    n_local = planes.shape[1]
+    st = np.zeros((n_local, STATE_WORDS[variant]), dtype=np.uint32)
+    st[:, : planes.shape[0]] = planes.T
+    return st

@@ -1,0 +1,512 @@
+/*
+ * ciprng_oracle.c -- the CPU ORACLE for the chaotic-iteration PRNG hot path
+ * of arXiv 1112.5239 (Bahi, Couturier, Guyeux, Heam).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1112_5239_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant generator with the
+ * CUDA path: every constant below is re-derived here from the paper or from
+ * the DESIGN.md reading it cites.
+ *
+ * Plain, slow, obviously-correct C99: scalar, single-threaded, no blocking,
+ * no fusion, no intrinsics.  Rounds of the neighbour-combined variants are
+ * simulated group by group in lockstep, in the order the paper's pseudocode
+ * states them.
+ *
+ * Citations: "P:a-b" = /root/reference/PAPER.md lines a-b; "S:a-b" = SPEC.md;
+ * "Qn" = reading n of the ambiguity ledger (restated in
+ * DESIGN.md s3).
+ *
+ * Pinning (what fixes each function other than itself; tests/test_oracle_pins.py):
+ *   orc_xor_step          Table 1, P:799-815 (paper's worked example)
+ *   orc_xorshift32        Alg. 2; Marsaglia's published example
+ *   orc_xor64             Marsaglia 2003 published first output (cited P:845)
+ *   orc_xor128_32         Marsaglia 2003 published first output (cited P:951)
+ *   orc_xor128_64/xorwow_64  hand-traced tiny-state steps (tests/golden/)
+ *   orc_splitmix_word     published SplitMix64 sequence (Q11)
+ *   orc_v0_*              hand-traced first output from a tiny state
+ *   orc_v1_*              hand-traced C=2 lockstep trace (S:355 tables),
+ *                         invariants I1 (prefix-XOR), I2 (self-cancel),
+ *                         I3 (group parity), I4 (split invariance)
+ *   orc_v2_*              BBS brute force, hand-traced
+ *                         C=1 trace, I6 closure, I7 rotation order 8
+ *   orc_stats_words       brute-force recount on tiny inputs; pi estimate
+ *   orc_digest_words      parity unpinned (a verification hash defined by
+ *                         this build; only its arithmetic is checked)
+ *   seeder/comb/modulus   parity unpinned by the paper: defined by this
+ *   table choices         build (Q6, Q11, Q13); the modulus table is pinned
+ *                         to P:1212-1214's constraints (primes = 3 mod 4,
+ *                         M < 2^16).
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <string.h>
+#include <stdlib.h>
+
+#define ORC_OK 0
+#define ORC_EINVAL (-1)
+
+/* ------------------------------------------------------------------------ */
+/* Eq. "Oplus": x^n = x^{n-1} XOR S^n.  The update of every      */
+/* variant.  Table 1 is its worked example.                      */
+/* ------------------------------------------------------------------------ */
+uint64_t orc_xor_step(uint64_t x, uint64_t s) { return x ^ s; }
+
+/* ------------------------------------------------------------------------ */
+/* Alg. 2, "An arbitrary round of XORshift", 32-bit, (13,17,5). */
+/* Not on the V0-V2 path under reading Q1; kept as the shift-convention pin. */
+/* ------------------------------------------------------------------------ */
+uint32_t orc_xorshift32(uint32_t *z)
+{
+    uint32_t v = *z;
+    v = v ^ (v << 13);
+    v = v ^ (v >> 17);
+    v = v ^ (v << 5);
+    *z = v;
+    return v;
+}
+
+/* ------------------------------------------------------------------------ */
+/* The three "classical 64-bits PRNGs" of Listing 1, Marsaglia  */
+/* 2003 recurrences on 64-bit words (readings Q1-A, Q2, Q3).                 */
+/* ------------------------------------------------------------------------ */
+
+/* xorshift == Marsaglia xor64, triple (13, 7, 17) (Q1 reading A). */
+uint64_t orc_xor64(uint64_t *a)
+{
+    uint64_t v = *a;
+    v ^= v << 13;
+    v ^= v >> 7;
+    v ^= v << 17;
+    *a = v;
+    return v;
+}
+
+/* xor128 on u64 words: t=(x^(x<<11)); x=y; y=z; z=w; w=(w^(w>>19))^(t^(t>>8)) (Q2). */
+uint64_t orc_xor128_64(uint64_t b[4])
+{
+    uint64_t t = b[0] ^ (b[0] << 11);
+    b[0] = b[1];
+    b[1] = b[2];
+    b[2] = b[3];
+    b[3] = (b[3] ^ (b[3] >> 19)) ^ (t ^ (t >> 8));
+    return b[3];
+}
+
+/* xorwow on u64 words: t=(x^(x>>2)); x=y; y=z; z=w; w=v;
+ * v=(v^(v<<4))^(t^(t<<1)); return (d+=362437)+v;  (Q2, Q3) */
+uint64_t orc_xorwow_64(uint64_t c[5], uint64_t *d)
+{
+    uint64_t t = c[0] ^ (c[0] >> 2);
+    c[0] = c[1];
+    c[1] = c[2];
+    c[2] = c[3];
+    c[3] = c[4];
+    c[4] = (c[4] ^ (c[4] << 4)) ^ (t ^ (t << 1));
+    *d = *d + 362437u;
+    return *d + c[4];
+}
+
+/* xor128 with "unsigned longs (64 bits) replaced by unsigned integers (32
+ * bits)" -- the strategy source of Alg. 4 (reading Q5). */
+uint32_t orc_xor128_32(uint32_t b[4])
+{
+    uint32_t t = b[0] ^ (b[0] << 11);
+    b[0] = b[1];
+    b[1] = b[2];
+    b[2] = b[3];
+    b[3] = (b[3] ^ (b[3] >> 19)) ^ (t ^ (t >> 8));
+    return b[3];
+}
+
+/* ------------------------------------------------------------------------ */
+/* Seeder (reading Q11): replaces the host ISAAC initialisation. */
+/* W(seed, s, k) = output number 16*s+k+1 of SplitMix64 started at `seed`.   */
+/* ------------------------------------------------------------------------ */
+uint64_t orc_mix64(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t orc_splitmix_word(uint64_t seed, uint64_t s, uint32_t k)
+{
+    uint64_t counter = 16u * s + (uint64_t)k + 1u;
+    return orc_mix64(seed + 0x9E3779B97F4A7C15ull * counter);
+}
+
+static uint32_t lo32(uint64_t v) { return (uint32_t)(v & 0xFFFFFFFFu); }
+static uint32_t hi32(uint64_t v) { return (uint32_t)(v >> 32); }
+
+/* ======================================================================== */
+/* V0: Listing 1 run per thread == Alg. 3 "naive" kernel.        */
+/* ======================================================================== */
+typedef struct {
+    uint64_t a;     /* xorshift (xor64) state               */
+    uint64_t b[4];  /* xor128 state (x, y, z, w)            */
+    uint64_t c[5];  /* xorwow shift registers (x, y, z, w, v) */
+    uint64_t d;     /* xorwow Weyl counter                  */
+    uint32_t x;     /* chaotic-iteration state       */
+    uint32_t pad;   /* always 0                             */
+} orc_v0_state;
+
+/* Per-stream initial state (Q11, Q12).  paper_defaults reproduces Listing 1
+ * (x = 123123123) with Marsaglia's published seeds. */
+void orc_v0_init_one(uint64_t seed, uint64_t s, int paper_defaults, orc_v0_state *st)
+{
+    int k;
+    memset(st, 0, sizeof(*st));
+    if (paper_defaults) {
+        st->a = 88172645463325252ull;
+        st->b[0] = 123456789u; st->b[1] = 362436069u; st->b[2] = 521288629u; st->b[3] = 88675123u;
+        st->c[0] = 123456789u; st->c[1] = 362436069u; st->c[2] = 521288629u; st->c[3] = 88675123u;
+        st->c[4] = 5783321u;
+        st->d = 6615241u;
+        st->x = 123123123u;
+        return;
+    }
+    st->a = orc_splitmix_word(seed, s, 0);
+    if (st->a == 0) st->a = 88172645463325252ull;              /* zero is a fixed point */
+    for (k = 0; k < 4; k++) st->b[k] = orc_splitmix_word(seed, s, 1 + k);
+    if ((st->b[0] | st->b[1] | st->b[2] | st->b[3]) == 0) {
+        st->b[0] = 123456789u; st->b[1] = 362436069u; st->b[2] = 521288629u; st->b[3] = 88675123u;
+    }
+    for (k = 0; k < 5; k++) st->c[k] = orc_splitmix_word(seed, s, 5 + k);
+    if ((st->c[0] | st->c[1] | st->c[2] | st->c[3] | st->c[4]) == 0) {
+        st->c[0] = 123456789u; st->c[1] = 362436069u; st->c[2] = 521288629u; st->c[3] = 88675123u;
+        st->c[4] = 5783321u;
+    }
+    st->d = orc_splitmix_word(seed, s, 10);
+    st->x = lo32(orc_splitmix_word(seed, s, 11));
+}
+
+/* One call of Listing 1: returns the new x. */
+uint32_t orc_v0_next(orc_v0_state *st)
+{
+    uint64_t t1 = orc_xor64(&st->a);
+    uint64_t t2 = orc_xor128_64(st->b);
+    uint64_t t3 = orc_xorwow_64(st->c, &st->d);
+    uint32_t x = st->x;
+    x = x ^ lo32(t1);
+    x = x ^ hi32(t2);
+    x = x ^ hi32(t3);
+    x = x ^ lo32(t2);
+    x = x ^ hi32(t1);
+    x = x ^ lo32(t3);
+    st->x = x;
+    return x;
+}
+
+/* ======================================================================== */
+/* V1: Alg. 4 "improved" kernel, lockstep two-phase (Q7).        */
+/* ======================================================================== */
+typedef struct {
+    uint32_t g[4];  /* xor128-32 state (x, y, z, w) */
+    uint32_t x;     /* chaotic-iteration state       */
+    uint32_t tp;    /* this thread's shared cell: previous round's t (Q8) */
+} orc_v1_state;
+
+void orc_v1_init_one(uint64_t seed, uint64_t s, orc_v1_state *st)
+{
+    int k;
+    for (k = 0; k < 4; k++) st->g[k] = lo32(orc_splitmix_word(seed, s, k));
+    if ((st->g[0] | st->g[1] | st->g[2] | st->g[3]) == 0) {
+        st->g[0] = 123456789u; st->g[1] = 362436069u; st->g[2] = 521288629u; st->g[3] = 88675123u;
+    }
+    st->x = lo32(orc_splitmix_word(seed, s, 4));
+    st->tp = lo32(orc_splitmix_word(seed, s, 5));
+}
+
+/* ======================================================================== */
+/* V2: Alg. 5 BBS kernel.                                      */
+/* ======================================================================== */
+typedef struct {
+    uint32_t y[8];  /* BBS internal states bbs1..bbs8                 */
+    uint32_t m[8];  /* index of each instance's modulus in orc_moduli */
+    uint32_t x;     /* chaotic-iteration state                        */
+    uint32_t tp;    /* shared cell (previous round's t)               */
+} orc_v2_state;
+
+/* Modulus table (Q13): "prime numbers around 256 that are congruent to 3
+ * modulus 4" with M = p*q < 2^16.  Primes p = 3 mod 4 in
+ * [128, 256]; all products p < q, ascending. */
+static uint32_t orc_moduli_tab[128];
+static int orc_moduli_n = 0;
+
+static int is_prime(uint32_t v)
+{
+    uint32_t d;
+    if (v < 2) return 0;
+    for (d = 2; d * d <= v; d++)
+        if (v % d == 0) return 0;
+    return 1;
+}
+
+static void build_moduli(void)
+{
+    uint32_t primes[64];
+    int np = 0, i, j, n = 0;
+    uint32_t v;
+    if (orc_moduli_n) return;
+    for (v = 128; v <= 256; v++)
+        if (is_prime(v) && v % 4 == 3) primes[np++] = v;
+    for (i = 0; i < np; i++)
+        for (j = i + 1; j < np; j++) orc_moduli_tab[n++] = primes[i] * primes[j];
+    /* insertion sort, ascending */
+    for (i = 1; i < n; i++) {
+        uint32_t key = orc_moduli_tab[i];
+        j = i - 1;
+        while (j >= 0 && orc_moduli_tab[j] > key) { orc_moduli_tab[j + 1] = orc_moduli_tab[j]; j--; }
+        orc_moduli_tab[j + 1] = key;
+    }
+    orc_moduli_n = n;
+}
+
+int orc_moduli(uint32_t *out, int cap)
+{
+    int i;
+    build_moduli();
+    for (i = 0; i < orc_moduli_n && i < cap; i++) out[i] = orc_moduli_tab[i];
+    return orc_moduli_n;
+}
+
+static uint32_t gcd32(uint32_t a, uint32_t b)
+{
+    while (b) { uint32_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+/* One BBS step x_{n+1} = x_n^2 mod M; x < M < 2^16 so x^2 < 2^32. */
+uint32_t orc_bbs_step(uint32_t y, uint32_t M) { return (y * y) % M; }
+
+/* Q21 seed: y = r^2 mod M with gcd(r, M) = 1 and y not in {0, 1}. */
+void orc_v2_init_one(uint64_t seed, uint64_t s, orc_v2_state *st)
+{
+    int j;
+    build_moduli();
+    for (j = 0; j < 8; j++) {
+        uint64_t w = orc_splitmix_word(seed, s, (uint32_t)j);
+        uint32_t mi = hi32(w) % (uint32_t)orc_moduli_n;
+        uint32_t M = orc_moduli_tab[mi];
+        uint32_t r = 2u + lo32(w) % (M - 3u);
+        while (gcd32(r, M) != 1u || (r * r) % M <= 1u) r = (r == M - 2u) ? 2u : r + 1u;
+        st->y[j] = (r * r) % M;
+        st->m[j] = mi;
+    }
+    st->x = lo32(orc_splitmix_word(seed, s, 8));
+    st->tp = lo32(orc_splitmix_word(seed, s, 9));
+}
+
+/* ======================================================================== */
+/* Grid-level entry points (the oracle's mirror of the C-ABI).              */
+/* variant: 0 = V0, 1 = V1, 2 = V2.  states: array of n_local per-stream    */
+/* structs of the variant's type.  Output is stream-major out[s*n + i] (Q9). */
+/* ======================================================================== */
+size_t orc_state_size(int variant)
+{
+    if (variant == 0) return sizeof(orc_v0_state);
+    if (variant == 1) return sizeof(orc_v1_state);
+    if (variant == 2) return sizeof(orc_v2_state);
+    return 0;
+}
+
+int orc_grid_init(int variant, uint64_t seed, uint64_t first_stream, uint64_t n_local,
+                  int paper_defaults, void *states)
+{
+    uint64_t s;
+    if (variant == 0) {
+        orc_v0_state *st = (orc_v0_state *)states;
+        if (paper_defaults && !(first_stream == 0 && n_local == 1)) return ORC_EINVAL;
+        for (s = 0; s < n_local; s++) orc_v0_init_one(seed, first_stream + s, paper_defaults, &st[s]);
+        return ORC_OK;
+    }
+    if (paper_defaults) return ORC_EINVAL;
+    if (variant == 1) {
+        orc_v1_state *st = (orc_v1_state *)states;
+        for (s = 0; s < n_local; s++) orc_v1_init_one(seed, first_stream + s, &st[s]);
+        return ORC_OK;
+    }
+    if (variant == 2) {
+        orc_v2_state *st = (orc_v2_state *)states;
+        for (s = 0; s < n_local; s++) orc_v2_init_one(seed, first_stream + s, &st[s]);
+        return ORC_OK;
+    }
+    return ORC_EINVAL;
+}
+
+/* Default combination arrays for C = 32 (reading Q6): the paper never prints
+ * array_comb1/2 or the 16 BBS arrangement arrays. */
+static void default_comb_v1(uint32_t l, uint32_t *c1, uint32_t *c2)
+{
+    *c1 = (l + 1u) % 32u;
+    *c2 = (l + 17u) % 32u;
+}
+
+static uint32_t default_comb_v2(uint32_t a, uint32_t l)
+{
+    if (a < 8u) return (l + 1u + a) % 32u;
+    return (l + 17u + (a - 8u)) % 32u;
+}
+
+/* V0 generate: each stream runs Listing 1 n times (Alg. 3). */
+static void v0_generate(orc_v0_state *st, uint64_t n_local, uint64_t n, uint32_t *out)
+{
+    uint64_t s, i;
+    for (s = 0; s < n_local; s++)
+        for (i = 0; i < n; i++) out[s * n + i] = orc_v0_next(&st[s]);
+}
+
+/* V1 generate (Alg. 4), per group of C streams, lockstep:
+ *   offset = threadIdx % C; o1 = threadIdx - offset + array_comb1[offset];
+ *   o2 likewise with array_comb2;
+ *   per round: t = xor-like(); t ^= shmem[o1] ^ shmem[o2]; shmem[tid] = t;
+ *   x ^= t; store x.
+ * Two-phase (Q7): every lane reads the previous round's shmem before any
+ * lane writes. */
+static int v1_generate(orc_v1_state *st, uint64_t n_local, uint32_t C, const uint8_t *comb,
+                       uint64_t n, uint32_t *out)
+{
+    uint64_t g0, i;
+    uint32_t l;
+    uint32_t gval[32], tnew[32], o1[32], o2[32];
+    if (C == 0 || C > 32 || n_local % C) return ORC_EINVAL;
+    if (comb == NULL && C != 32) return ORC_EINVAL;
+    for (l = 0; l < C; l++) {
+        if (comb) { o1[l] = comb[l]; o2[l] = comb[C + l]; }
+        else default_comb_v1(l, &o1[l], &o2[l]);
+        if (o1[l] >= C || o2[l] >= C) return ORC_EINVAL;
+    }
+    for (g0 = 0; g0 < n_local; g0 += C) {
+        orc_v1_state *grp = &st[g0];
+        for (i = 0; i < n; i++) {
+            /* phase 1: every thread draws its xor-like number */
+            for (l = 0; l < C; l++) gval[l] = orc_xor128_32(grp[l].g);
+            /* phase 2: combine with the previous round's shared cells */
+            for (l = 0; l < C; l++) tnew[l] = gval[l] ^ grp[o1[l]].tp ^ grp[o2[l]].tp;
+            /* phase 3: commit shared cells, chaotic-iteration update, store */
+            for (l = 0; l < C; l++) {
+                grp[l].tp = tnew[l];
+                grp[l].x = orc_xor_step(grp[l].x, tnew[l]);
+                out[(g0 + l) * n + i] = grp[l].x;
+            }
+        }
+    }
+    return ORC_OK;
+}
+
+/* V2 generate (Alg. 5), per group of C streams, lockstep.
+ * o1, o2 chosen once per call from the call-entry states of bbs1, bbs2
+ * (Q15: array_comb[8 + (bbs2 & 7)], Q16).  Per round: 8 squarings give 8
+ * nibbles; bbs3 and bbs7 give two shifts of at most 3 bits,
+ * filled with exactly `shift` low bits of new bbs1 / bbs2 draws
+ * (Q17, Q18); then the combination and update as in V1.
+ * At the end of the call the 8 (state, modulus) pairs rotate: instance j
+ * is stored in place j+1, instance 8 in place 1 (Q19, Q20). */
+static int v2_generate(orc_v2_state *st, uint64_t n_local, uint32_t C, const uint8_t *comb,
+                       uint64_t n, uint32_t *out)
+{
+    static const uint32_t array_shift[4] = {0u, 1u, 3u, 7u};
+    uint64_t g0, i;
+    uint32_t l, a;
+    uint32_t tnew[32], o1[32], o2[32];
+    uint32_t tab[16][32];
+    build_moduli();
+    if (C == 0 || C > 32 || n_local % C) return ORC_EINVAL;
+    if (comb == NULL && C != 32) return ORC_EINVAL;
+    for (a = 0; a < 16; a++)
+        for (l = 0; l < C; l++) {
+            tab[a][l] = comb ? comb[a * C + l] : default_comb_v2(a, l);
+            if (tab[a][l] >= C) return ORC_EINVAL;
+        }
+    if (n == 0) return ORC_OK; /* no launch, no rotation (Q20) */
+    for (g0 = 0; g0 < n_local; g0 += C) {
+        orc_v2_state *grp = &st[g0];
+        for (l = 0; l < C; l++) {
+            o1[l] = tab[grp[l].y[0] & 7u][l];
+            o2[l] = tab[8u + (grp[l].y[1] & 7u)][l];
+        }
+        for (i = 0; i < n; i++) {
+            for (l = 0; l < C; l++) {
+                orc_v2_state *p = &grp[l];
+                uint32_t t = 0, shift, j;
+                for (j = 0; j < 8; j++) {
+                    p->y[j] = orc_bbs_step(p->y[j], orc_moduli_tab[p->m[j]]);
+                    t = (t << 4) | (p->y[j] & 15u);
+                }
+                p->y[2] = orc_bbs_step(p->y[2], orc_moduli_tab[p->m[2]]);
+                shift = p->y[2] & 3u;
+                t = t << shift;
+                p->y[0] = orc_bbs_step(p->y[0], orc_moduli_tab[p->m[0]]);
+                t = t | (p->y[0] & array_shift[shift]);
+                p->y[6] = orc_bbs_step(p->y[6], orc_moduli_tab[p->m[6]]);
+                shift = p->y[6] & 3u;
+                t = t << shift;
+                p->y[1] = orc_bbs_step(p->y[1], orc_moduli_tab[p->m[1]]);
+                t = t | (p->y[1] & array_shift[shift]);
+                tnew[l] = t;
+            }
+            for (l = 0; l < C; l++) tnew[l] = tnew[l] ^ grp[o1[l]].tp ^ grp[o2[l]].tp;
+            for (l = 0; l < C; l++) {
+                grp[l].tp = tnew[l];
+                grp[l].x = orc_xor_step(grp[l].x, tnew[l]);
+                out[(g0 + l) * n + i] = grp[l].x;
+            }
+        }
+        /* rotation: place j+1 <- instance j, place 1 <- instance 8 */
+        for (l = 0; l < C; l++) {
+            orc_v2_state *p = &grp[l];
+            uint32_t y7 = p->y[7], m7 = p->m[7];
+            int j;
+            for (j = 7; j > 0; j--) { p->y[j] = p->y[j - 1]; p->m[j] = p->m[j - 1]; }
+            p->y[0] = y7;
+            p->m[0] = m7;
+        }
+    }
+    return ORC_OK;
+}
+
+int orc_grid_generate(int variant, void *states, uint64_t n_local, uint32_t C,
+                      const uint8_t *comb, uint64_t n, uint32_t *out)
+{
+    if (variant == 0) { v0_generate((orc_v0_state *)states, n_local, n, out); return ORC_OK; }
+    if (variant == 1) return v1_generate((orc_v1_state *)states, n_local, C, comb, n, out);
+    if (variant == 2) return v2_generate((orc_v2_state *)states, n_local, C, comb, n, out);
+    return ORC_EINVAL;
+}
+
+/* ======================================================================== */
+/* Consumer statistics (reading Q24; the paper only says numbers can be      */
+/* "consumed directly after generation").                       */
+/* stats[0] += #pairs with u^2 + v^2 < 2^64, u = x_{2k}, v = x_{2k+1} of one */
+/* stream within one call; stats[1] += #pairs; stats[2 + (x >> 24)] += 1.    */
+/* ======================================================================== */
+int orc_stats_words(const uint32_t *out, uint64_t n_local, uint64_t n, uint64_t *stats)
+{
+    uint64_t s, i;
+    if (n % 2) return ORC_EINVAL;
+    for (s = 0; s < n_local; s++) {
+        for (i = 0; i < n; i++) stats[2 + (out[s * n + i] >> 24)] += 1;
+        for (i = 0; i + 1 < n; i += 2) {
+            uint64_t u = out[s * n + i], v = out[s * n + i + 1];
+            uint64_t uu = u * u, vv = v * v;
+            stats[1] += 1;
+            if (vv <= ~uu) stats[0] += 1; /* u^2 + v^2 <= 2^64 - 1 */
+        }
+    }
+    return ORC_OK;
+}
+
+/* Verification digest (reading Q28): sum over the call's words of
+ * mix64(mix64(idx) ^ x_idx) mod 2^64, idx = (first_stream + s) * n + i. */
+uint64_t orc_digest_words(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n)
+{
+    uint64_t s, i, acc = 0;
+    for (s = 0; s < n_local; s++)
+        for (i = 0; i < n; i++) {
+            uint64_t idx = (first_stream + s) * n + i;
+            acc += orc_mix64(orc_mix64(idx) ^ (uint64_t)out[s * n + i]);
+        }
+    return acc;
+}

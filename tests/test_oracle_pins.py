@@ -1,0 +1,376 @@
+"""Pins of the CPU oracle to things other than itself (not gpu).
+
+Each test names what fixes the value: the paper's worked example, a published
+sequence of a generator the paper cites, a hand trace under tests/golden/, an
+invariant the paper states, a special case, or brute force.  Readings Qn are
+listed in DESIGN.md s3.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from tests import statcheck
+
+M32 = 0xFFFFFFFF
+
+
+# ---------------------------------------------------------------- Eq. Oplus
+def test_table1_round(golden):
+    """Table 1: the paper's worked x XOR S^i."""
+    g = golden["table1"]
+    x, s, r = (int(g[k], 2) for k in ("x", "S", "x_xor_S"))
+    assert O.xor_step(x, s) == r
+
+
+def test_oplus_special_cases():
+    """x ^ 0 = x; (x ^ s) ^ s = x; exactly the bits set in S flip."""
+    gen = W.rng(1)
+    for x, s in W.random_words(gen, (64, 2)).tolist():
+        assert O.xor_step(x, 0) == x
+        assert O.xor_step(O.xor_step(x, s), s) == x
+        assert bin(O.xor_step(x, s) ^ x).count("1") == bin(s).count("1")
+
+
+# ------------------------------------------------------- strategy sources
+def test_xorshift32_alg2(golden):
+    p = golden["published_sequences"]
+    for key in ("xorshift32_13_17_5", "xorshift32_from_1"):
+        e = p[key]
+        assert O.xorshift32_seq(e["seed"], len(e["outputs"])) == e["outputs"]
+
+
+def test_xor64_published(golden):
+    e = golden["published_sequences"]["xor64"]
+    assert O.xor64_seq(e["seed"], len(e["outputs"])) == e["outputs"]
+
+
+def test_xor128_32_published(golden):
+    e = golden["published_sequences"]["xor128_32"]
+    assert O.xor128_32_seq(e["seed"], len(e["outputs"])) == e["outputs"]
+
+
+def test_xor128_64_and_xorwow_64_hand(golden):
+    h = golden["hand_traces"]
+    e = h["xor128_64_tiny"]
+    assert O.xor128_64_seq(e["state"], 2) == e["outputs"]
+    e = h["xorwow_64_tiny"]
+    assert O.xorwow_64_seq(e["state"], e["d"], 2) == e["outputs"]
+
+
+# ----------------------------------------------------------------- seeder
+def test_splitmix_published(golden):
+    e = golden["published_sequences"]["splitmix64"]
+    assert [O.splitmix_word(e["seed"], 0, k) for k in range(5)] == e["outputs"]
+
+
+def test_splitmix_counter_structure():
+    """W(seed, s, k) is output 16*s+k+1 of one SplitMix64 sequence: the word
+    for (s, k) equals the word for (0, 16*s + k) (Q11; stream-count invariance
+    rests on this)."""
+    for s in (1, 7, 12345):
+        for k in (0, 5, 15):
+            assert O.splitmix_word(99, s, k) == O.splitmix_word(99, 0, 16 * s + k)
+    assert O.mix64(0) == 0  # fixed point of the finaliser
+
+
+# --------------------------------------------------------------------- V0
+def _v0_state(a, b, c, d, x):
+    st = np.zeros((1, 24), dtype=np.uint32)
+    for i, v in enumerate([a, *b, *c, d]):
+        st[0, 2 * i] = v & M32
+        st[0, 2 * i + 1] = v >> 32
+    st[0, 22] = x
+    return st
+
+
+def test_v0_hand_trace(golden):
+    e = golden["hand_traces"]["v0_tiny_first_output"]
+    s = e["state"]
+    st = _v0_state(s["a"], s["b"], s["c"], s["d"], s["x"])
+    assert O.generate(O.V0, st, 1)[0].tolist() == e["outputs"]
+
+
+def test_v0_paper_defaults_is_listing1_fold():
+    """I1 for V0: x_i ^ x_{i-1} = lo^hi fold of the three pinned generators
+    (Listing 1), starting from x = 123123123."""
+    n = 64
+    st = O.init_states(O.V0, 0, 0, 1, paper_defaults=True)
+    out = O.generate(O.V0, st, n)[0].astype(np.uint64)
+    t1 = O.xor64_seq(88172645463325252, n)
+    t2 = O.xor128_64_seq([123456789, 362436069, 521288629, 88675123], n)
+    t3 = O.xorwow_64_seq([123456789, 362436069, 521288629, 88675123, 5783321], 6615241, n)
+    prev = 123123123
+    for i in range(n):
+        f = 0
+        for t in (t1[i], t2[i], t3[i]):
+            f ^= (t & M32) ^ (t >> 32)
+        assert int(out[i]) == prev ^ f
+        prev = int(out[i])
+
+
+def test_v0_split_invariance():
+    """I4: generate(a+b) == generate(a) ++ generate(b) (state persists)."""
+    st1 = O.init_states(O.V0, 5, 0, 3)
+    st2 = st1.copy()
+    full = O.generate(O.V0, st1, 10)
+    part = np.concatenate([O.generate(O.V0, st2, 4), O.generate(O.V0, st2, 6)], axis=1)
+    assert np.array_equal(full, part)
+    assert np.array_equal(st1, st2)
+
+
+def test_v0_paper_defaults_needs_single_stream():
+    with pytest.raises(O.OracleError):
+        O.init_states(O.V0, 0, 0, 2, paper_defaults=True)
+
+
+# --------------------------------------------------------------------- V1
+def test_v1_hand_trace_c2(golden):
+    e = golden["hand_traces"]["v1_c2_trace"]
+    st = np.array([[*ln["xor128"], ln["x"], ln["tp"]] for ln in e["lanes"]], dtype=np.uint32)
+    comb = np.array(e["comb1"] + e["comb2"], dtype=np.uint8)
+    out = O.generate(O.V1, st, 3, comb_size=2, comb=comb)
+    assert out.tolist() == e["outputs"]
+
+
+def test_v1_self_combination_is_prefix_xor_of_xor128(golden):
+    """I2 + I1: with C = 1 (o1 = o2 = self) the shared terms cancel,
+    so x_i = x_{i-1} ^ xor128(), the published Marsaglia sequence."""
+    seeds = golden["published_sequences"]["xor128_32"]["seed"]
+    x0 = 0xDEADBEEF
+    st = np.array([[*seeds, x0, 0x12345678]], dtype=np.uint32)
+    out = O.generate(O.V1, st, 5, comb_size=1, comb=np.array([0, 0], dtype=np.uint8))[0]
+    assert int(out[0]) == x0 ^ golden["published_sequences"]["xor128_32"]["outputs"][0]
+    g = O.xor128_32_seq(seeds, 5)
+    prev = x0
+    for i in range(5):
+        assert int(out[i]) == prev ^ g[i]
+        prev = int(out[i])
+
+
+def _xor128_streams(st, n):
+    return np.array([O.xor128_32_seq(row[:4].tolist(), n) for row in st], dtype=np.uint64)
+
+
+@pytest.mark.parametrize("custom", [False, True])
+def test_v1_group_parity(custom):
+    """I3: comb1, comb2 are permutations, so every previous-round t is used
+    exactly twice per group and XOR over lanes of t_i equals XOR over lanes of
+    the xor-like draws g_i; with I1 (x_i ^ x_{i-1} = t_i) this is checkable
+    from the outputs and the pinned xor128 alone."""
+    gen = W.rng(3)
+    S, n = 64, 9
+    st = O.init_states(O.V1, 77, 0, S)
+    x0 = st[:, 4].astype(np.uint64)
+    comb = W.random_comb(gen, 32, 2) if custom else None
+    g = _xor128_streams(st, n)
+    out = O.generate(O.V1, st.copy(), n, comb=comb).astype(np.uint64)
+    t = out ^ np.concatenate([x0[:, None], out[:, :-1]], axis=1)
+    for grp in range(S // 32):
+        sl = slice(32 * grp, 32 * grp + 32)
+        assert np.array_equal(np.bitwise_xor.reduce(t[sl], axis=0), np.bitwise_xor.reduce(g[sl], axis=0))
+
+
+def test_v1_default_tables_plus1_plus17():
+    """Reading Q6: the default arrays are comb1[l] = l+1, comb2[l] = l+17 (mod
+    32).  Inject a single non-zero shared cell at lane k: in round 0 exactly
+    lanes k-1 and k-17 see it (t = g ^ shmem[o1] ^ shmem[o2])."""
+    S = 32
+    st = O.init_states(O.V1, 1, 0, S)
+    st[:, 4] = 0
+    st[:, 5] = 0
+    k, T = 20, 0xA5A5A5A5
+    st[k, 5] = T
+    g = _xor128_streams(st, 1)[:, 0]
+    out = O.generate(O.V1, st, 1)[:, 0].astype(np.uint64)
+    seen = {l for l in range(S) if int(out[l] ^ g[l]) == T}
+    zero = {l for l in range(S) if int(out[l] ^ g[l]) == 0}
+    assert seen == {(k - 1) % 32, (k - 17) % 32}
+    assert zero == set(range(S)) - seen
+
+
+def test_v1_split_invariance():
+    st1 = O.init_states(O.V1, 9, 0, 64)
+    st2 = st1.copy()
+    full = O.generate(O.V1, st1, 13)
+    part = np.concatenate([O.generate(O.V1, st2, 5), O.generate(O.V1, st2, 8)], axis=1)
+    assert np.array_equal(full, part) and np.array_equal(st1, st2)
+
+
+def test_v1_shard_invariance():
+    """I5: per-stream seeding makes a shard's output its slice of the whole."""
+    whole = O.generate(O.V1, O.init_states(O.V1, 4, 0, 128), 7)
+    hi = O.generate(O.V1, O.init_states(O.V1, 4, 64, 64), 7)
+    assert np.array_equal(whole[64:], hi)
+
+
+def test_v1_config_errors():
+    st = O.init_states(O.V1, 0, 0, 33)
+    with pytest.raises(O.OracleError):
+        O.generate(O.V1, st, 1)  # incomplete group
+    st = O.init_states(O.V1, 0, 0, 4)
+    with pytest.raises(O.OracleError):
+        O.generate(O.V1, st, 1, comb_size=4, comb=np.array([0, 1, 2, 4, 0, 1, 2, 3], np.uint8))
+    with pytest.raises(O.OracleError):
+        O.generate(O.V1, st, 1, comb_size=4)  # defaults exist for C = 32 only
+
+
+# --------------------------------------------------------------------- V2
+def _v2_state(y, midx, x, tp):
+    return np.array([[*y, *midx, x, tp]], dtype=np.uint32)
+
+
+def test_bbs_small(golden):
+    for c in golden["hand_traces"]["bbs_small"]["cases"]:
+        y, orbit = c["y"], []
+        for _ in c["orbit"]:
+            y = O.bbs_step(y, c["M"])
+            orbit.append(y)
+        assert orbit == c["orbit"]
+
+
+def test_modulus_table_constraints():
+    """Q13 / P:1212-1214: products of two distinct primes = 3 (mod 4) 'around
+    256', M < 2^16, so x^2 < 2^32 with 32-bit arithmetic."""
+    mods = O.moduli()
+    primes = [p for p in range(128, 257) if all(p % d for d in range(2, int(p**0.5) + 1)) and p % 4 == 3]
+    assert len(primes) == 13 and len(mods) == 78 == math.comb(13, 2)
+    assert mods == sorted(mods) and mods[0] == 131 * 139 and mods[-1] == 239 * 251 == 59989
+    for M in mods:
+        assert M < 2**16 and (M - 1) ** 2 < 2**32
+        fac = [p for p in primes if M % p == 0]
+        assert len(fac) == 2 and fac[0] * fac[1] == M
+
+
+def test_v2_hand_trace_c1(golden):
+    e = golden["hand_traces"]["v2_c1_trace"]
+    midx = O.moduli().index(e["M"])
+    st = _v2_state(e["y"], [midx] * 8, e["x"], e["tp"])
+    out = O.generate(O.V2, st, 2, comb_size=1, comb=np.zeros(16, np.uint8))
+    assert out[0].tolist() == e["outputs"]
+    assert st[0, :8].tolist() == e["y_after_call"]
+
+
+def test_v2_rotation_direction():
+    """'internal variable for BBS number 1 is stored in place 2,
+    ..., BBS number 8 is stored in place 1' -- and the modulus moves with it
+    (Q19).  Per round instances 1, 2, 3, 7 are drawn twice, the others once
+    (P:1269-1280)."""
+    mods = O.moduli()
+    st = O.init_states(O.V2, 11, 0, 32)
+    before = st.copy()
+    O.generate(O.V2, st, 1)
+    draws = [2, 2, 2, 1, 1, 1, 2, 1]
+    for s in range(32):
+        for j in range(8):
+            y, m = int(before[s, j]), int(before[s, 8 + j])
+            for _ in range(draws[j]):
+                y = y * y % mods[m]
+            assert int(st[s, (j + 1) % 8]) == y and int(st[s, 8 + (j + 1) % 8]) == m
+
+
+def test_v2_zero_rounds_no_rotation():
+    st = O.init_states(O.V2, 2, 0, 32)
+    before = st.copy()
+    out = O.generate(O.V2, st, 0)
+    assert out.shape == (32, 0) and np.array_equal(st, before)
+
+
+def test_v2_state_invariants():
+    """I6: 1 < y < M-1, gcd(y, M) = 1, y^2 < 2^32, across calls."""
+    mods = O.moduli()
+    st = O.init_states(O.V2, 3, 0, 64)
+    for _ in range(20):
+        for row in st:
+            for j in range(8):
+                y, M = int(row[j]), mods[int(row[8 + j])]
+                assert 1 < y < M - 1 and math.gcd(y, M) == 1 and y * y < 2**32
+        O.generate(O.V2, st, 37)
+
+
+def test_v2_selection_uses_call_entry_states():
+    """Q15/Q16: o1 = comb[bbs1 & 7], o2 = comb[8 + (bbs2 & 7)]
+    with the call-entry states; default arrays are l+1+a and l+17+a (Q6).
+    Inject one non-zero shared cell at lane k and predict who sees it."""
+    st = O.init_states(O.V2, 21, 0, 32)
+    st[:, 16] = 0
+    st[:, 17] = 0
+    k, T = 5, 0x5A5A5A5A
+    st[k, 17] = T
+    entry = st.copy()
+    # each lane's own strategy word from a self-cancelling C=1 run (pinned above)
+    own = np.zeros(32, dtype=np.uint64)
+    for l in range(32):
+        one = entry[l : l + 1].copy()
+        one[0, 17] = 0
+        own[l] = O.generate(O.V2, one, 1, comb_size=1, comb=np.zeros(16, np.uint8))[0, 0]
+    out = O.generate(O.V2, st, 1)[:, 0].astype(np.uint64)
+    for l in range(32):
+        o1 = (l + 1 + (int(entry[l, 0]) & 7)) % 32
+        o2 = (l + 17 + (int(entry[l, 1]) & 7)) % 32
+        expect = (T if o1 == k else 0) ^ (T if o2 == k else 0)
+        assert int(out[l] ^ own[l]) == expect
+
+
+def test_v2_not_split_invariant():
+    """I4 negative: selection and rotation happen per call (P:1224-1230,
+    P:1287), so two calls of 3 differ from one call of 6."""
+    st1 = O.init_states(O.V2, 8, 0, 32)
+    st2 = st1.copy()
+    full = O.generate(O.V2, st1, 6)
+    part = np.concatenate([O.generate(O.V2, st2, 3), O.generate(O.V2, st2, 3)], axis=1)
+    assert np.array_equal(full[:, :3], part[:, :3])
+    assert not np.array_equal(full, part)
+
+
+# ------------------------------------------------------------ consumer stats
+def test_stats_brute_force():
+    gen = W.rng(5)
+    words = W.random_words(gen, (7, 10))
+    words[0, 0], words[0, 1] = 0xFFFFFFFF, 0  # boundary pair: u^2 < 2^64
+    words[1, 0], words[1, 1] = 0xFFFFFFFF, 1  # u^2 + v^2 > 2^64 - 1? check exactly
+    st = O.stats(words)
+    inside = pairs = 0
+    hist = [0] * 256
+    for row in words.tolist():
+        for v in row:
+            hist[v >> 24] += 1
+        for i in range(0, len(row), 2):
+            pairs += 1
+            inside += row[i] ** 2 + row[i + 1] ** 2 < 2**64
+    assert int(st[0]) == inside and int(st[1]) == pairs and st[2:].tolist() == hist
+
+
+def test_stats_odd_n_rejected():
+    with pytest.raises(O.OracleError):
+        O.stats(np.zeros((2, 3), np.uint32))
+
+
+@pytest.mark.parametrize("variant", [O.V0, O.V1, O.V2])
+def test_oracle_output_statistics(variant):
+    """Frequency / runs / byte chi-square sanity (stand-in for BigCrush,
+    P:851-853) and the Monte-Carlo pi estimate within 5 sigma."""
+    S, n = (32, 4096) if variant else (8, 16384)
+    st = O.init_states(variant, W.SEEDS[0], 0, S)
+    out = O.generate(variant, st, n)
+    assert statcheck.passes(statcheck.battery(out))
+    s = O.stats(out)
+    assert abs(statcheck.pi_zscore(int(s[0]), int(s[1]))) < 5
+    assert 1e-4 < statcheck.hist_chi2_p(s[2:]) < 1 - 1e-4
+
+
+def test_statcheck_negative_controls():
+    """all-zero and alternating streams must fail."""
+    assert not statcheck.passes(statcheck.battery(np.zeros(4096, np.uint32)))
+    assert not statcheck.passes(statcheck.battery(np.full(4096, 0x55555555, np.uint32)))
+
+
+def test_digest_shard_additive():
+    """Q28: the digest is a position-aware sum, so shard digests add mod 2^64."""
+    out = O.generate(O.V1, O.init_states(O.V1, 1, 0, 64), 8)
+    assert O.digest(out) == (O.digest(out[:32]) + O.digest(out[32:], 32)) % 2**64
+    swapped = out.copy()
+    swapped[[0, 1]] = swapped[[1, 0]]
+    assert O.digest(swapped) != O.digest(out)
