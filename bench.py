@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the chaotic-iteration PRNG hot path (arXiv 1112.5239) on B200.
+
+Metric (BASELINE.json): 32-bit random numbers/s, whole job, and the fraction
+of the HBM write roofline.  One step = one prng_generate call of BASELINE
+configs[1] per GPU: V1 (Alg. 4, xor128 + neighbour combination), 2^20 streams
+x 128 numbers, stored to HBM (512 MiB per step, > 126 MB L2, so no L2 flush
+is needed).  Multi-GPU (torchrun, one process per GPU): every rank owns 2^20
+consecutive streams of one global stream space (weak scaling); the store path
+has no collective at all.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/, plain single-threaded C) on
+this host on a bounded sample of the same workload: the paper ships no code,
+so the oracle is the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "32-bit random numbers/sec at 1/2/4/8 B200; % of HBM write roofline"
+UNIT = "numbers/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+CFG = W.CONFIGS["C2"]
+S_PER_GPU, N_PER_STREAM = CFG["n_streams"], CFG["n"]
+STATE_BYTES_V1 = 24  # per stream, read once + written once per call
+
+
+def env_rank():
+    r = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    lr = int(os.environ.get("LOCAL_RANK", str(r)))
+    return r, ws, lr
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)", d
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the V1 store kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_v1_store.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """NVML clock / throttle-reason sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def time_oracle(seconds: float = 10.0, max_calls: int = 64):
+    """The oracle as it stands, single thread, on the C2 workload (full 2^20
+    streams x 128 per call), as many calls as fit in ~`seconds`."""
+    import oracle as O
+
+    st = O.init_states(W.V1, W.SEEDS[0], 0, S_PER_GPU)
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        O.generate(W.V1, st, N_PER_STREAM)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or calls >= max_calls:
+            break
+    numbers = calls * S_PER_GPU * N_PER_STREAM
+    return {
+        "value": numbers / el,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": "oracle",
+        "sample": f"{calls} call(s) of the full C2 workload (V1, 2^20 streams x 128) = {numbers} numbers, "
+                  f"single-threaded C oracle, {el:.1f} s wall",
+    }
+
+
+# --------------------------------------------------------------------------
+def run_reference(args):
+    rank, ws, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle as O
+
+    # bounded sample per step: 2^15 streams x 128 of the C2 workload (~40 ms)
+    S_s = 2**15
+    st = O.init_states(W.V1, W.SEEDS[0], 0, S_s)
+    for _ in range(args.warmup):
+        O.generate(W.V1, st, N_PER_STREAM)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.generate(W.V1, st, N_PER_STREAM)
+    el = time.perf_counter() - t0
+    v = args.steps * S_s * N_PER_STREAM / el
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded)",
+        "config": {"workload": "C2 sample: V1 xor128 + neighbour combination, 2^15 streams x 128 numbers per step "
+                               "(bounded sample of 2^20 x 128)", "variant": "v1"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} steps x 2^15 streams x 128 numbers, single-threaded C oracle"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1112_5239_b200 as P
+
+    rank, ws, lr = env_rank()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(lr)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    else:
+        torch.cuda.set_device(lr)
+        dist = None
+    dev = torch.device("cuda", lr)
+    S, n = S_PER_GPU, N_PER_STREAM
+    g = P.ChaoticPRNG(W.SEEDS[0], S * ws, P.V1, shard=(rank * S, S), store_path=args.store_path)
+    out = torch.empty((S, n), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        g.generate(n, out=out)
+    launches_per_step = g.info().kernel_launches
+    store_path_used = g.info().store_path
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(lr) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            g.generate(n, out=out)
+            evs[k][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    numbers = args.steps * S * n * ws
+    value = numbers / (total_ms / 1e3)
+
+    # ---- end-to-end through the public API with a pinned host buffer
+    host = torch.empty((S, n), dtype=torch.int32, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    g.generate_host(n, out=host)  # warm (staging buffers, copy stream)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        g.generate_host(n, out=host)
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    e2e_value = e2e_steps * S * n * ws / e2e_s
+
+    # ---- roofline of the dominant (only) kernel
+    peak, peak_src, peaks = measured_peaks()
+    alg_bytes = 4 * S * n + 2 * STATE_BYTES_V1 * S
+    avg_kern_s = statistics.mean(kern_ms) / 1e3
+    achieved = alg_bytes / avg_kern_s / 1e9
+    traffic = ncu_traffic()
+
+    secondary = {}
+    if not args.no_secondary:
+        secondary = measure_secondary(P, torch, dev, args)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded; SplitMix64 per-stream seeding, seed 0x0123456789ABCDEF)",
+        "config": {
+            "workload": "C2 (BASELINE configs[1]): V1 Alg.4 xor128 + neighbour combination (default C=32 arrays), "
+                        f"{S} streams x {n} numbers per GPU per step, stored to HBM",
+            "variant": "v1",
+            "streams_per_gpu": S,
+            "n_per_stream": n,
+            "global_streams": S * ws,
+            "store_path": {1: "direct", 2: "tma"}.get(store_path_used, str(store_path_used)),
+            "l2": "output 512 MiB per step per GPU > 126 MB L2 (inputs larger than L2, no flush)",
+            "parallelism": f"stream-sharded x{ws} (no collective on the store path)",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "kernel": "v1_fast_kernel<StoreSink>",
+            "alg_bytes_per_launch": alg_bytes,
+            "avg_kernel_ms": avg_kern_s * 1e3,
+            "peak_source": peak_src,
+        },
+        "e2e": {
+            "value": e2e_value,
+            "unit": UNIT,
+            "h2d_bytes_per_step": 0,
+            "d2h_bytes_per_step": 4 * S * n,
+            "api": "prng_generate_host (pinned host buffer, chunked generate + D2H overlap)",
+            "steps": e2e_steps,
+        },
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    if secondary:
+        line["secondary"] = secondary
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = time_oracle(args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_secondary(P, torch, dev, args):
+    """Other rows of SURVEY s8(a) on this GPU (not the headline): V2 store
+    (C3), V0 store and V1 fused consumer; numbers/s with CUDA events."""
+    res = {}
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, steps):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / steps
+
+    S, n = W.CONFIGS["C3"]["n_streams"], W.CONFIGS["C3"]["n"]
+    g = P.ChaoticPRNG(W.SEEDS[0], S, P.V2)
+    out = torch.empty((S, n), dtype=torch.int32, device=dev)
+    s = timed(lambda: g.generate(n, out=out), 20)
+    res["c3_v2_store"] = {"value": S * n / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S, "n": n}
+    g.close()
+    S0, n0 = 2**20, 128
+    g = P.ChaoticPRNG(W.SEEDS[0], S0, P.V0)
+    out = torch.empty((S0, n0), dtype=torch.int32, device=dev)
+    s = timed(lambda: g.generate(n0, out=out), 20)
+    res["v0_store"] = {"value": S0 * n0 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S0, "n": n0}
+    g.close()
+    del out
+    S5, n5 = 2**20, 1024
+    g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)
+    s = timed(lambda: g.consume(n5, stats), 10)
+    res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
+    g.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--store-path", type=int, default=0, help="0 auto, 1 direct STG, 2 TMA tiles")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,217 @@
+/*
+ * ciprng.h -- C ABI of the B200-native chaotic-iteration PRNG hot path
+ * (arXiv 1112.5239, Bahi, Couturier, Guyeux, Heam).
+ *
+ * One handle = the persistent per-thread state of the paper's GPU kernels
+ * ("InternalVarXorLikeArray" / "InternalVarBBSArray", P:895-905, P:959-978,
+ * P:1254-1287) for a contiguous range of streams (one stream = one paper
+ * thread), resident in HBM of the device that was current at creation.
+ *
+ * Citations: P:a-b = PAPER.md lines a-b; Qn = reading n of the ambiguity
+ * ledger, DESIGN.md s3.
+ *
+ * Conventions for every entry point
+ *  - Returns PRNG_OK (0) or a negative prng_status; never throws, never
+ *    aborts.  PRNG_ECUDA carries a CUDA error (prng_last_cuda_error() gives
+ *    its text); asynchronous kernel faults surface at the next synchronising
+ *    call.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device-pointer calls only ENQUEUE work on `stream` and return
+ *    immediately; handle state updates are stream-ordered.
+ *  - A handle is single-owner: concurrent calls on one handle (from several
+ *    host threads or on several streams without ordering) are undefined
+ *    (SPEC S:85-86).  Distinct handles are independent.
+ *  - Pointers named *_dev are device pointers (e.g. a torch tensor's
+ *    data_ptr()); *_host are host pointers; the caller owns both.
+ */
+#ifndef CIPRNG_H
+#define CIPRNG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CIPRNG_API __attribute__((visibility("default")))
+#else
+#define CIPRNG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct prng_s prng_t; /* opaque; owns the device state */
+
+/* Variants:
+ *  V0  Listing 1 per thread = Alg. 3 "naive" kernel:
+ *      three 64-bit xor-like generators (xor64, xor128, xorwow; readings
+ *      Q1-A, Q2, Q3); x ^= lo(t1)^hi(t2)^hi(t3)^lo(t2)^hi(t1)^lo(t3).
+ *  V1  Alg. 4 "improved" kernel: one 32-bit xor128 per thread
+ *      (Q5); t = xor128() ^ shmem[o1] ^ shmem[o2]; shmem[tid] = t; x ^= t.
+ *  V2  Alg. 5 BBS kernel: 8 Blum-Blum-Shub instances, 4 low
+ *      bits per squaring, two variable shifts, 16 arrangement arrays chosen
+ *      per call, state rotation at exit. */
+enum prng_variant {
+    PRNG_V0_XORLIKE3 = 0,
+    PRNG_V1_XOR128_COMB = 1,
+    PRNG_V2_BBS_COMB = 2
+};
+
+enum prng_status {
+    PRNG_OK = 0,
+    PRNG_EINVAL = -1,  /* bad argument / configuration                */
+    PRNG_ENOMEM = -2,  /* device or host allocation failed            */
+    PRNG_ECUDA = -3,   /* CUDA runtime / driver error                 */
+    PRNG_EALIGN = -4,  /* out_dev not 16-byte aligned when required   */
+    PRNG_ESIZE = -5,   /* size overflow (n * n_local * 4 > SIZE_MAX)   */
+    PRNG_ESTATE = -6   /* state buffer size mismatch (get/set_state)  */
+};
+
+/* Store path of prng_generate (tuning knob; every path is bit-identical). */
+enum prng_store_path {
+    PRNG_STORE_AUTO = 0,   /* TMA tiles when possible, else direct        */
+    PRNG_STORE_DIRECT = 1, /* per-thread 128-bit STG of 4-round buffers   */
+    PRNG_STORE_TMA = 2     /* warp tiles staged in shared memory, written
+                              by cp.async.bulk.tensor (V1 default tables,
+                              n % 4 == 0); falls back to DIRECT otherwise */
+};
+
+typedef struct prng_config {
+    /* combination_size C (reading Q6): 0 = default 32.
+     * Must be 1, 2, 4, 8, 16 or 32 (a group never straddles a warp). */
+    uint32_t comb_size;
+    /* HOST pointer, copied at creation.  V1: 2*C entries, array_comb1 then
+     * array_comb2.  V2: 16*C entries, array_comb[0..15][0..C-1]
+     * row-major.  Each entry < C.  NULL = the default tables, which
+     * exist for C = 32 only (Q6): V1 comb1[l] = l+1, comb2[l] = l+17 (mod
+     * 32); V2 array_comb[a][l] = l+1+a, array_comb[8+a][l] = l+17+a (mod 32),
+     * a = 0..7.  Ignored by V0. */
+    const uint8_t *comb;
+    /* V0 with a single stream only: Listing 1's initial state (x =
+     * 123123123, with Marsaglia's published seeds; Q12). */
+    int32_t paper_defaults;
+    /* enum prng_store_path */
+    int32_t store_path;
+} prng_config;
+
+/* ---------------------------------------------------------------------- */
+/* Lifetime                                                               */
+/* ---------------------------------------------------------------------- */
+
+/* prng_create(seed, n_streams, variant, &h) == prng_create_shard(seed, 0,
+ * n_streams, variant, NULL, &h).  Synchronous (returns with the state
+ * initialised on the current device). */
+CIPRNG_API int prng_create(uint64_t seed, uint64_t n_streams, int variant, prng_t **out);
+
+/* Create the handle for global streams [first_stream, first_stream+n_local)
+ * of the stream space seeded by `seed`.  The state of global stream s is a
+ * pure function of (seed, s, variant) (seeder, reading Q11: SplitMix64
+ * counter words W(seed, s, k)), so the output of stream s never depends on
+ * how streams are sharded over handles or GPUs.
+ * Errors: PRNG_EINVAL if variant unknown, n_local == 0, out == NULL,
+ * comb_size not a power of two <= 32, a table entry >= C, comb == NULL with
+ * C != 32, V1/V2 with first_stream % C or n_local % C != 0 (groups must be
+ * complete), paper_defaults with anything but V0 and
+ * (first_stream, n_local) == (0, 1) (Q26). PRNG_ENOMEM, PRNG_ECUDA. */
+CIPRNG_API int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, int variant,
+                      const prng_config *cfg, prng_t **out);
+
+/* Frees the device state and any staging buffers.  NULL is a no-op.
+ * Synchronises with outstanding work of the handle's internal streams. */
+CIPRNG_API int prng_destroy(prng_t *h);
+
+/* ---------------------------------------------------------------------- */
+/* Hot path                                                               */
+/* ---------------------------------------------------------------------- */
+
+/* One kernel call of n_per_stream rounds on every stream of the handle
+ * (Alg. 3 / 4 / 5 "for i=1 to n"): each round draws
+ * the strategy word t, combines it with the group's previous-round shared
+ * cells (V1, V2), applies x ^= t (Eq. "Oplus") and emits x.
+ * Output layout (reading Q9): stream-major, out_dev[s_local*n + i] is round
+ * i of local stream s_local; n_local*n u32 words, caller-owned.  State is
+ * written back at the end; V2 rotates its 8 BBS instances
+ * (Q19, Q20).  n_per_stream == 0: no-op, no launch,
+ * no V2 rotation.  V0/V1 are chunk-split invariant: generate(a+b) ==
+ * generate(a) ++ generate(b) row-wise; V2 is not (its arrangement arrays are
+ * chosen per call).
+ * Errors: PRNG_EINVAL (h NULL, or out_dev NULL with n > 0), PRNG_ESIZE, PRNG_EALIGN (the TMA
+ * store path requires 16-byte alignment; other paths fall back to scalar
+ * stores when out_dev or n is not 16-byte friendly), PRNG_ECUDA. */
+CIPRNG_API int prng_generate(prng_t *h, uint64_t n_per_stream, uint32_t *out_dev, void *stream);
+
+/* Same words as prng_generate, written to a HOST buffer (n_local*n u32,
+ * stream-major).  Generation runs on `stream` in stream-range chunks into
+ * two device staging buffers owned by the handle while the previous chunk
+ * is copied device->host on an internal copy stream.  Pinned host memory is
+ * strongly recommended (pageable memory works but copies synchronously).
+ * SYNCHRONOUS: returns after the last word has landed in out_host. */
+CIPRNG_API int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *out_host, void *stream);
+
+/* Fused consumer mode (the paper removes the store; statistics
+ * are reading Q24): run the same n rounds as prng_generate -- identical
+ * state evolution -- but use every x in-kernel instead of storing it, and
+ * ADD into stats_dev[258] (u64, caller-zeroed):
+ *   [0] pairs (u, v) = (x_{2k}, x_{2k+1}) of one stream within the call with
+ *       u^2 + v^2 < 2^64 (Monte-Carlo pi: pi ~ 4*[0]/[1]);
+ *   [1] number of pairs = n_local * n / 2;
+ *   [2 + b] count of x with x >> 24 == b, b = 0..255.
+ * Integer sums, so results are independent of launch shape and of how
+ * streams are sharded (the multi-GPU all-reduce is bit-exact).
+ * Errors: PRNG_EINVAL if n is odd or a pointer is NULL, PRNG_ECUDA. */
+CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
+
+/* Verification digest of one call's output block (reading Q28):
+ * digest_dev[0] += sum over s < n_local, i < n of
+ *   mix64(mix64((first_stream + s) * n + i) ^ out_dev[s*n + i])  (mod 2^64),
+ * mix64 = SplitMix64 finaliser.  Position-aware and additive across shards. */
+CIPRNG_API int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n,
+                uint64_t *digest_dev, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Introspection, checkpoint / test hooks                                 */
+/* ---------------------------------------------------------------------- */
+
+typedef struct prng_info_t {
+    int32_t variant;
+    uint32_t comb_size;
+    uint64_t seed, first_stream, n_local;
+    uint32_t state_words; /* u32 planes per stream (V0 23, V1 6, V2 18) */
+    int32_t device;
+    int32_t store_path;   /* path used by the last prng_generate */
+    uint32_t kernel_launches; /* kernels launched by the last call */
+} prng_info_t;
+
+CIPRNG_API int prng_get_info(const prng_t *h, prng_info_t *info);
+
+/* State layout (SoA u32 planes; plane k of local stream s at word
+ * k*n_local + s):
+ *  V0 (23): a.lo a.hi | b0.lo b0.hi .. b3.lo b3.hi | c0.lo c0.hi .. c4.lo c4.hi
+ *           | d.lo d.hi | x        (xor64 a; xor128 b; xorwow c and Weyl d)
+ *  V1 (6):  xor128 x y z w | x | tp  (tp = this stream's shared cell, Q8)
+ *  V2 (18): y1..y8 (BBS states) | m1..m8 (index of each instance's modulus
+ *           in the ascending table of the 78 products p*q, p < q primes = 3
+ *           mod 4 in [128, 256], Q13) | x | tp
+ * get/set copy exactly state_words*n_local*4 bytes (else PRNG_ESTATE) and
+ * synchronise the device.  set_state is the checkpoint-resume hook (P:905:
+ * the state written back after every kernel is a checkpoint). */
+CIPRNG_API int prng_get_state(const prng_t *h, void *host_buf, size_t bytes);
+CIPRNG_API int prng_set_state(prng_t *h, const void *host_buf, size_t bytes);
+
+CIPRNG_API const char *prng_strerror(int status);
+CIPRNG_API const char *prng_last_cuda_error(void);
+
+/* Host-side exhaustive self-check of the kernels' division-free BBS squaring
+ * (Barrett, P:1209-1211 asks for 32-bit modulus only): for every modulus of
+ * the table and every y < M, compares with y*y % M.  Writes the number of
+ * mismatches; runs on the CPU (no GPU needed). */
+CIPRNG_API int prng_selftest_modsq(uint64_t *mismatches);
+
+/* Library build string (compiler, arch). */
+CIPRNG_API const char *prng_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CIPRNG_H */

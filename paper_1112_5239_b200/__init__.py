@@ -1,0 +1,152 @@
+"""B200-native chaotic-iteration PRNG (arXiv 1112.5239) -- Python binding.
+
+``ChaoticPRNG`` wraps one C-ABI handle (include/ciprng.h).  PyTorch supplies
+device memory, streams and (for multi-GPU) the process group; every step of
+the hot path -- seeding, strategy generation, neighbour combination, the
+chaotic-iteration update, stores or the fused consumer -- runs in this
+package's sm_100a kernels (csrc/).  Importing works on a CPU-only host (the
+library loads), but every compute call needs a CUDA device: there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from ._lib import (  # noqa: F401
+    STORE_AUTO,
+    STORE_DIRECT,
+    STORE_TMA,
+    PrngConfig,
+    PrngError,
+    PrngInfo,
+    check,
+    declared_symbols,
+    lib,
+)
+
+V0, V1, V2 = 0, 1, 2
+STATE_WORDS = {V0: 23, V1: 6, V2: 18}
+N_STATS = 258
+
+__all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "STATE_WORDS", "N_STATS", "lib", "PrngError"]
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class ChaoticPRNG:
+    """Per-stream chaotic-iteration generators for global streams
+    [first, first + n_local) of the stream space of ``seed``.
+
+    variant: V0 (Listing 1 / Alg. 3), V1 (Alg. 4), V2 (Alg. 5, BBS).
+    comb_size / comb: combination arrays (None = default C = 32 tables).
+    """
+
+    def __init__(self, seed: int, n_streams: int, variant: int = V1, *, shard: tuple[int, int] | None = None,
+                 comb_size: int | None = None, comb=None, paper_defaults: bool = False,
+                 store_path: int = STORE_AUTO, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ChaoticPRNG needs a CUDA device (sm_100a); there is no CPU fallback")
+        self.variant = variant
+        self.seed = seed & (2**64 - 1)
+        first, n_local = shard if shard is not None else (0, n_streams)
+        self.first, self.n_local, self.n_streams = first, n_local, n_streams
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+        self._comb = None if comb is None else np.ascontiguousarray(comb, dtype=np.uint8)
+        cfg = PrngConfig(
+            comb_size=comb_size or 0,
+            comb=None if self._comb is None else self._comb.ctypes.data,
+            paper_defaults=int(paper_defaults),
+            store_path=store_path,
+        )
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(lib().prng_create_shard(self.seed, first, n_local, variant, ctypes.byref(cfg), ctypes.byref(h)),
+                  "prng_create_shard")
+        self._h = h
+
+    # ----------------------------------------------------------------- hot path
+    def generate(self, n: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """One call of n rounds; returns int32 [n_local, n] (bit pattern = u32)."""
+        if out is None:
+            out = torch.empty((self.n_local, n), dtype=torch.int32, device=self.device)
+        assert out.is_cuda and out.is_contiguous() and out.numel() >= self.n_local * n and out.element_size() == 4
+        check(lib().prng_generate(self._h, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+              "prng_generate")
+        return out
+
+    def generate_host(self, n: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Same words into a (pinned) host tensor, overlapping D2H with generation."""
+        if out is None:
+            out = torch.empty((self.n_local, n), dtype=torch.int32, pin_memory=True)
+        assert not out.is_cuda and out.is_contiguous() and out.numel() >= self.n_local * n
+        check(lib().prng_generate_host(self._h, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+              "prng_generate_host")
+        return out
+
+    def consume(self, n: int, stats: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Fused consumer: adds {inside, pairs, hist[256]} into int64 [258] (u64 bits)."""
+        if stats is None:
+            stats = torch.zeros(N_STATS, dtype=torch.int64, device=self.device)
+        assert stats.is_cuda and stats.numel() == N_STATS and stats.dtype == torch.int64
+        check(lib().prng_consume(self._h, n, ctypes.c_void_p(stats.data_ptr()), _stream_handle(stream)),
+              "prng_consume")
+        return stats
+
+    # ------------------------------------------------------------ introspection
+    def info(self) -> PrngInfo:
+        inf = PrngInfo()
+        check(lib().prng_get_info(self._h, ctypes.byref(inf)), "prng_get_info")
+        return inf
+
+    def get_state(self) -> np.ndarray:
+        """SoA state planes, uint32 [state_words, n_local] (include/ciprng.h)."""
+        buf = np.zeros((STATE_WORDS[self.variant], self.n_local), dtype=np.uint32)
+        check(lib().prng_get_state(self._h, ctypes.c_void_p(buf.ctypes.data), buf.nbytes), "prng_get_state")
+        return buf
+
+    def set_state(self, planes: np.ndarray) -> None:
+        buf = np.ascontiguousarray(planes, dtype=np.uint32)
+        check(lib().prng_set_state(self._h, ctypes.c_void_p(buf.ctypes.data), buf.nbytes), "prng_set_state")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().prng_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def digest(out: torch.Tensor, first_stream: int = 0, acc: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Position-aware verification digest of a [n_local, n] output block (Q28)."""
+    n_local, n = out.shape
+    if acc is None:
+        acc = torch.zeros(1, dtype=torch.int64, device=out.device)
+    check(lib().prng_digest(ctypes.c_void_p(out.data_ptr()), first_stream, n_local, n,
+                            ctypes.c_void_p(acc.data_ptr()), _stream_handle(stream)), "prng_digest")
+    return acc
+
+
+def as_u32(t: torch.Tensor) -> np.ndarray:
+    """Copy a device/host int32 tensor to a numpy uint32 array (bit-exact)."""
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def as_u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64)

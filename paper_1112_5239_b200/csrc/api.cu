@@ -1,0 +1,472 @@
+// api.cu -- the C ABI of include/ciprng.h: argument checking, device state
+// ownership, kernel-path selection and the pipelined device->host path.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ciprng.h"
+#include "device.cuh"
+#include "kernels.h"
+
+#define CIPRNG_STR_(x) #x
+#define CIPRNG_STR(x) CIPRNG_STR_(x)
+
+using namespace ciprng;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "no error";
+
+int cuda_fail(cudaError_t e) {
+    std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return PRNG_ECUDA;
+}
+#define CK(expr)                                   \
+    do {                                           \
+        cudaError_t e_ = (expr);                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Modulus table of V2 (reading Q13), built here independently of any other
+// component: primes p = 3 (mod 4) in [128, 256] by a sieve, products p < q
+// ascending, each with its Barrett constant mu = floor(2^32 / M).
+std::vector<uint32_t> modulus_table() {
+    std::vector<bool> composite(257, false);
+    std::vector<uint32_t> primes;
+    for (uint32_t v = 2; v <= 256; ++v) {
+        if (composite[v]) continue;
+        for (uint32_t w = v * v; w <= 256; w += v) composite[w] = true;
+        if (v >= 128 && (v & 3u) == 3u) primes.push_back(v);
+    }
+    std::vector<uint32_t> Ms;
+    for (size_t i = 0; i < primes.size(); ++i)
+        for (size_t k = i + 1; k < primes.size(); ++k) Ms.push_back(primes[i] * primes[k]);
+    std::sort(Ms.begin(), Ms.end());
+    std::vector<uint32_t> tab;
+    for (uint32_t M : Ms) {
+        tab.push_back(M);
+        tab.push_back((uint32_t)((1ull << 32) / M));
+    }
+    return tab;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+constexpr int kStateWords[3] = {23, 6, 18};
+
+}  // namespace
+
+struct prng_s {
+    int variant = 0;
+    uint64_t seed = 0, first = 0, n_local = 0;
+    uint32_t C = 32;
+    bool default_tables = true;
+    int device = 0;
+    int store_path = PRNG_STORE_AUTO;
+    CombTables comb{};
+    uint32_t *state = nullptr;
+    uint32_t *mod = nullptr;  // V2 modulus table {M, mu} x n_mod
+    uint32_t n_mod = 0;
+    int num_sms = 148;
+    int persistent_blocks = 0;
+    // last call info
+    int last_path = 0;
+    uint32_t last_launches = 0;
+    // TMA descriptor cache
+    struct TmEntry {
+        const void *ptr = nullptr;
+        uint64_t n = 0, rows = 0;
+        CUtensorMap map;
+        bool ok = false;
+    } tm[4];
+    int tm_next = 0;
+    // host pipeline
+    uint32_t *staging[2] = {nullptr, nullptr};
+    size_t staging_words = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_gen[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+const CUtensorMap *tensor_map(prng_t *h, const uint32_t *out, uint64_t n, uint64_t rows) {
+    for (auto &e : h->tm)
+        if (e.ok && e.ptr == out && e.n == n && e.rows == rows) return &e.map;
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return nullptr;
+    auto &e = h->tm[h->tm_next];
+    h->tm_next = (h->tm_next + 1) & 3;
+    cuuint64_t gdim[2] = {n, rows};
+    cuuint64_t gstride[1] = {n * 4};
+    cuuint32_t box[2] = {16, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t *>(out), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    e.ok = (r == CUDA_SUCCESS);
+    e.ptr = out;
+    e.n = n;
+    e.rows = rows;
+    return e.ok ? &e.map : nullptr;
+}
+
+// Enqueue one pass over local streams [s_begin, s_begin + s_count).
+// mode 0 = store to out, 2 = consume into stats.
+int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t *out, uint64_t *stats, int mode,
+             cudaStream_t st) {
+    GenArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.state = h->state;
+    a.n_local = h->n_local;
+    a.s_begin = s_begin;
+    a.s_count = s_count;
+    a.n = n;
+    a.out = out;
+    a.stats = stats;
+    a.mod = h->mod;
+    a.C = h->C;
+    a.comb = h->comb;
+    a.vec = (out != nullptr && (n % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0)) ? 1u : 0u;
+    int launches = 0;
+    int path = PRNG_STORE_DIRECT;
+    if (h->variant == 0) {
+        launches = launch_v0(a, mode, st, h->persistent_blocks);
+    } else if (h->variant == 1) {
+        const bool fast = h->default_tables && h->C == 32;
+        int kmode = mode;
+        const CUtensorMap *tm = nullptr;
+        if (mode == 0 && fast) {
+            const bool tma_ok = a.vec && n < (1ull << 31) && s_count < (1ull << 31);
+            if (h->store_path == PRNG_STORE_TMA && reinterpret_cast<uintptr_t>(out) % 16 != 0) return PRNG_EALIGN;
+            if (h->store_path != PRNG_STORE_DIRECT && tma_ok) {
+                tm = tensor_map(h, out, n, s_count);
+                if (tm) {
+                    kmode = 1;
+                    path = PRNG_STORE_TMA;
+                }
+            }
+        }
+        launches = launch_v1(a, fast, kmode, tm, st, h->persistent_blocks);
+    } else {
+        launches = launch_v2(a, mode, st, h->persistent_blocks);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+    h->last_launches += launches;
+    h->last_path = path;
+    return PRNG_OK;
+}
+
+bool pow2_le32(uint32_t c) { return c >= 1 && c <= 32 && (c & (c - 1)) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int prng_create(uint64_t seed, uint64_t n_streams, int variant, prng_t **out) {
+    return prng_create_shard(seed, 0, n_streams, variant, nullptr, out);
+}
+
+int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, int variant, const prng_config *cfg,
+                      prng_t **out) {
+    if (out == nullptr) return PRNG_EINVAL;
+    *out = nullptr;
+    if (variant < 0 || variant > 2 || n_local == 0) return PRNG_EINVAL;
+    uint32_t C = 32;
+    const uint8_t *comb = nullptr;
+    int paper_defaults = 0, store_path = PRNG_STORE_AUTO;
+    if (cfg) {
+        if (cfg->comb_size) C = cfg->comb_size;
+        comb = cfg->comb;
+        paper_defaults = cfg->paper_defaults;
+        store_path = cfg->store_path;
+    }
+    if (store_path < 0 || store_path > 2) return PRNG_EINVAL;
+    if (paper_defaults && !(variant == 0 && first_stream == 0 && n_local == 1)) return PRNG_EINVAL;
+    if (n_local > (1ull << 40)) return PRNG_ESIZE;
+    prng_t *h = new (std::nothrow) prng_t();
+    if (!h) return PRNG_ENOMEM;
+    h->variant = variant;
+    h->seed = seed;
+    h->first = first_stream;
+    h->n_local = n_local;
+    h->store_path = store_path;
+    if (variant != 0) {
+        if (!pow2_le32(C) || first_stream % C || n_local % C || (comb == nullptr && C != 32)) {
+            delete h;
+            return PRNG_EINVAL;
+        }
+        const int ntab = variant == 1 ? 2 : 16;
+        for (int t = 0; t < ntab; ++t)
+            for (uint32_t l = 0; l < C; ++l) {
+                uint32_t v;
+                if (comb) {
+                    v = comb[t * C + l];
+                    if (v >= C) {
+                        delete h;
+                        return PRNG_EINVAL;
+                    }
+                } else if (variant == 1) {
+                    v = (t == 0) ? (l + 1u) % 32u : (l + 17u) % 32u;  // Q6
+                } else {
+                    v = (t < 8) ? (l + 1u + t) % 32u : (l + 17u + (t - 8)) % 32u;  // Q6
+                }
+                h->comb.t[t][l] = (uint8_t)v;
+            }
+        h->C = C;
+        h->default_tables = (comb == nullptr);
+    }
+    int rc = PRNG_OK;
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e);
+    }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->persistent_blocks = h->num_sms * 8;
+    const size_t words = (size_t)kStateWords[variant] * n_local;
+    e = cudaMalloc(&h->state, words * 4);
+    if (e != cudaSuccess) {
+        cuda_fail(e);
+        delete h;
+        return PRNG_ENOMEM;
+    }
+    std::vector<uint32_t> tab = modulus_table();
+    h->n_mod = (uint32_t)(tab.size() / 2);
+    e = cudaMalloc(&h->mod, tab.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(h->mod, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        rc = cuda_fail(e);
+        prng_destroy(h);
+        return rc;
+    }
+    InitArgs ia;
+    ia.state = h->state;
+    ia.n_local = n_local;
+    ia.seed = seed;
+    ia.first_stream = first_stream;
+    ia.variant = variant;
+    ia.paper_defaults = paper_defaults;
+    ia.mod = h->mod;
+    ia.n_mod = h->n_mod;
+    launch_init(ia, 0);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        rc = cuda_fail(e);
+        prng_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return PRNG_OK;
+}
+
+int prng_destroy(prng_t *h) {
+    if (!h) return PRNG_OK;
+    DeviceGuard g(h->device);
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    cudaFree(h->state);
+    cudaFree(h->mod);
+    cudaFree(h->staging[0]);
+    cudaFree(h->staging[1]);
+    for (int b = 0; b < 2; ++b) {
+        if (h->ev_gen[b]) cudaEventDestroy(h->ev_gen[b]);
+        if (h->ev_copy[b]) cudaEventDestroy(h->ev_copy[b]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    delete h;
+    return PRNG_OK;
+}
+
+static int check_size(const prng_t *h, uint64_t n) {
+    if (n && h->n_local > SIZE_MAX / 4 / n) return PRNG_ESIZE;
+    return PRNG_OK;
+}
+
+int prng_generate(prng_t *h, uint64_t n_per_stream, uint32_t *out_dev, void *stream) {
+    if (!h) return PRNG_EINVAL;
+    h->last_launches = 0;
+    if (n_per_stream == 0) return PRNG_OK;  // no words to write: out_dev may be NULL
+    if (!out_dev) return PRNG_EINVAL;
+    int rc = check_size(h, n_per_stream);
+    if (rc) return rc;
+    DeviceGuard g(h->device);
+    return run_pass(h, n_per_stream, 0, h->n_local, out_dev, nullptr, 0, (cudaStream_t)stream);
+}
+
+int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *out_host, void *stream) {
+    if (!h) return PRNG_EINVAL;
+    h->last_launches = 0;
+    if (n_per_stream == 0) return PRNG_OK;
+    if (!out_host) return PRNG_EINVAL;
+    int rc = check_size(h, n_per_stream);
+    if (rc) return rc;
+    DeviceGuard g(h->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    // chunk = whole 64-stream tiles, about 64 MiB of output
+    const uint64_t row_bytes = n_per_stream * 4;
+    uint64_t rows = (64ull << 20) / row_bytes;
+    rows = std::max<uint64_t>(64, rows / 64 * 64);
+    if (rows > h->n_local) rows = h->n_local;
+    const size_t need = (size_t)rows * n_per_stream;
+    if (need > h->staging_words) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(h->staging[b]);
+            h->staging[b] = nullptr;
+        }
+        h->staging_words = 0;
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaMalloc(&h->staging[b], need * 4);
+            if (e != cudaSuccess) {
+                cuda_fail(e);
+                return PRNG_ENOMEM;
+            }
+        }
+        h->staging_words = need;
+    }
+    if (!h->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&h->ev_gen[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_copy[b], cudaEventDisableTiming));
+        }
+    }
+    uint32_t launches = 0;
+    uint64_t chunk = 0;
+    for (uint64_t r0 = 0; r0 < h->n_local; r0 += rows, ++chunk) {
+        const int b = (int)(chunk & 1);
+        const uint64_t cnt = std::min<uint64_t>(rows, h->n_local - r0);
+        if (chunk >= 2) CK(cudaStreamWaitEvent(st, h->ev_copy[b], 0));
+        h->last_launches = 0;
+        rc = run_pass(h, n_per_stream, r0, cnt, h->staging[b], nullptr, 0, st);
+        if (rc) return rc;
+        launches += h->last_launches;
+        CK(cudaEventRecord(h->ev_gen[b], st));
+        CK(cudaStreamWaitEvent(h->copy_stream, h->ev_gen[b], 0));
+        CK(cudaMemcpyAsync(out_host + r0 * n_per_stream, h->staging[b], cnt * row_bytes, cudaMemcpyDeviceToHost,
+                           h->copy_stream));
+        CK(cudaEventRecord(h->ev_copy[b], h->copy_stream));
+    }
+    h->last_launches = launches;
+    CK(cudaStreamSynchronize(h->copy_stream));
+    CK(cudaStreamSynchronize(st));
+    return PRNG_OK;
+}
+
+int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream) {
+    if (!h || !stats_dev || (n_per_stream & 1)) return PRNG_EINVAL;
+    h->last_launches = 0;
+    if (n_per_stream == 0) return PRNG_OK;
+    DeviceGuard g(h->device);
+    return run_pass(h, n_per_stream, 0, h->n_local, nullptr, stats_dev, 2, (cudaStream_t)stream);
+}
+
+int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest_dev,
+                void *stream) {
+    if (!out_dev || !digest_dev) return PRNG_EINVAL;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    launch_digest(out_dev, first_stream, n_local, n, digest_dev, (cudaStream_t)stream, sms * 8);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
+}
+
+int prng_get_info(const prng_t *h, prng_info_t *info) {
+    if (!h || !info) return PRNG_EINVAL;
+    info->variant = h->variant;
+    info->comb_size = h->C;
+    info->seed = h->seed;
+    info->first_stream = h->first;
+    info->n_local = h->n_local;
+    info->state_words = (uint32_t)kStateWords[h->variant];
+    info->device = h->device;
+    info->store_path = h->last_path;
+    info->kernel_launches = h->last_launches;
+    return PRNG_OK;
+}
+
+int prng_get_state(const prng_t *h, void *host_buf, size_t bytes) {
+    if (!h || !host_buf) return PRNG_EINVAL;
+    const size_t need = (size_t)kStateWords[h->variant] * h->n_local * 4;
+    if (bytes != need) return PRNG_ESTATE;
+    DeviceGuard g(h->device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(host_buf, h->state, need, cudaMemcpyDeviceToHost));
+    return PRNG_OK;
+}
+
+int prng_set_state(prng_t *h, const void *host_buf, size_t bytes) {
+    if (!h || !host_buf) return PRNG_EINVAL;
+    const size_t need = (size_t)kStateWords[h->variant] * h->n_local * 4;
+    if (bytes != need) return PRNG_ESTATE;
+    DeviceGuard g(h->device);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(h->state, host_buf, need, cudaMemcpyHostToDevice));
+    return PRNG_OK;
+}
+
+const char *prng_strerror(int status) {
+    switch (status) {
+        case PRNG_OK: return "ok";
+        case PRNG_EINVAL: return "invalid argument or configuration";
+        case PRNG_ENOMEM: return "out of memory";
+        case PRNG_ECUDA: return "CUDA error (see prng_last_cuda_error)";
+        case PRNG_EALIGN: return "output pointer not 16-byte aligned";
+        case PRNG_ESIZE: return "size overflow";
+        case PRNG_ESTATE: return "state buffer size mismatch";
+        default: return "unknown status";
+    }
+}
+
+const char *prng_last_cuda_error(void) { return g_cuda_err; }
+
+int prng_selftest_modsq(uint64_t *mismatches) {
+    if (!mismatches) return PRNG_EINVAL;
+    std::vector<uint32_t> tab = modulus_table();
+    uint64_t bad = 0;
+    for (size_t k = 0; k + 1 < tab.size(); k += 2) {
+        const uint32_t M = tab[k], mu = tab[k + 1];
+        for (uint32_t y = 0; y < M; ++y)
+            if (barrett_sq(y, M, mu) != (y * y) % M) ++bad;
+    }
+    *mismatches = bad;
+    return PRNG_OK;
+}
+
+const char *prng_version(void) {
+    return "ciprng 0.1 (sm_100a; nvcc " CIPRNG_STR(__CUDACC_VER_MAJOR__) "." CIPRNG_STR(__CUDACC_VER_MINOR__) ")";
+}
+
+}  // extern "C"

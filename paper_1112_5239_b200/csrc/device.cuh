@@ -1,0 +1,135 @@
+// device.cuh -- sm_100a device primitives of the chaotic-iteration PRNG.
+//
+// Independent of oracle/ (no shared code or tables).  Citations: P:a-b =
+// PAPER.md lines; Qn = DESIGN.md s3 readings.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ciprng {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------- seeder
+// Q11: W(seed, s, k) = SplitMix64 output number 16 s + k + 1 from `seed`.
+__host__ __device__ __forceinline__ uint64_t splitmix_fin(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+__host__ __device__ __forceinline__ uint64_t seed_word(uint64_t seed, uint64_t s, uint32_t k) {
+    return splitmix_fin(seed + 0x9E3779B97F4A7C15ull * (s * 16u + k + 1u));
+}
+
+// ------------------------------------------------------- xor-like sources
+// Marsaglia xor128 on 32-bit words (Alg. 4 source), written as
+// the 4-term recurrence w_{k+4} = f(w_k, w_{k+3}) so an unroll-by-4 loop
+// keeps the state in a register ring with no moves.
+__device__ __forceinline__ uint32_t xor128_f(uint32_t xk, uint32_t wk3) {
+    uint32_t t = xk ^ (xk << 11);
+    return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
+}
+// Same on 64-bit words (Listing 1's xor128, reading Q2).
+__device__ __forceinline__ uint64_t xor128_f64(uint64_t xk, uint64_t wk3) {
+    uint64_t t = xk ^ (xk << 11);
+    return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
+}
+// xorwow shift register on 64-bit words: v_{k+5} = (v ^ v<<4) ^ (t ^ t<<1),
+// t = x ^ x>>2 with x = v_k, v = v_{k+4} (Q2, Q3).
+__device__ __forceinline__ uint64_t xorwow_f64(uint64_t xk, uint64_t vk4) {
+    uint64_t t = xk ^ (xk >> 2);
+    return (vk4 ^ (vk4 << 4)) ^ (t ^ (t << 1));
+}
+// Marsaglia xor64 (13, 7, 17) (Listing 1's xorshift, reading Q1-A).
+__device__ __forceinline__ uint64_t xor64_step(uint64_t a) {
+    a ^= a << 13;
+    a ^= a >> 7;
+    a ^= a << 17;
+    return a;
+}
+
+// --------------------------------------------------------------- BBS mod
+// Division-free x^2 mod M for M < 2^16 (P:1209-1214 wants 32-bit modular
+// arithmetic only).  Barrett: mu = floor(2^32 / M); for T = y*y < 2^32,
+// q = hi32(T * mu) is floor(T/M) or floor(T/M) - 1, so r = T - q*M < 2M and
+// one conditional subtraction (unsigned min) finishes.  Exhaustively checked
+// by prng_selftest_modsq() for every modulus and every y < M.
+__host__ __device__ __forceinline__ uint32_t barrett_sq(uint32_t y, uint32_t M, uint32_t mu) {
+    uint32_t T = y * y;
+#ifdef __CUDA_ARCH__
+    uint32_t q = __umulhi(T, mu);
+#else
+    uint32_t q = (uint32_t)(((uint64_t)T * mu) >> 32);
+#endif
+    uint32_t r = T - q * M;
+    uint32_t r2 = r - M;
+    return r2 < r ? r2 : r;  // r >= M  <=>  r - M does not wrap  <=>  r - M < r
+}
+
+// ---------------------------------------------------------------- stores
+__device__ __forceinline__ void st_v4(uint32_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+// ------------------------------------------------------------------- TMA
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t smem_addr, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_addr), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// --------------------------------------------------- consumer statistics
+// Q24: pair (u, v) is "inside" iff u^2 + v^2 < 2^64 <=> v^2 <= ~(u^2).
+__device__ __forceinline__ uint32_t pi_inside(uint32_t u, uint32_t v) {
+    uint64_t uu = (uint64_t)u * u, vv = (uint64_t)v * v;
+    return vv <= ~uu ? 1u : 0u;
+}
+
+// ------------------------------------------------------ kernel arguments
+struct CombTables {
+    uint8_t t[16][32];  // V1 uses rows 0 (array_comb1) and 1 (array_comb2)
+};
+
+struct GenArgs {
+    uint32_t *state;     // SoA planes, plane stride = n_local words
+    uint64_t n_local;    // plane stride
+    uint64_t s_begin;    // first local stream of this launch
+    uint64_t s_count;    // streams in this launch (multiple of C for V1/V2)
+    uint64_t n;          // rounds per stream
+    uint32_t *out;       // row 0 = stream s_begin; row stride n (store kernels)
+    uint64_t *stats;     // consume kernels: 258 u64
+    const uint32_t *mod; // V2: [78][2] = {M, mu}
+    uint32_t C;          // combination_size
+    uint32_t vec;        // 1: rows are 16-byte aligned, n % 4 == 0
+    CombTables comb;
+};
+
+}  // namespace ciprng

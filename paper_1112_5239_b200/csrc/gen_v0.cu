@@ -1,0 +1,113 @@
+// gen_v0.cu -- V0: Listing 1 run by every thread = Alg. 3 "naive" kernel
+// on sm_100a.
+//
+// Per stream: xor64 a (Q1-A), xor128 on u64 b0..b3 (Q2), xorwow on u64
+// c0..c4 + Weyl d (Q2, Q3), and x.  Per round:
+//   t1 = xorshift(); t2 = xor128(); t3 = xorwow();
+//   x ^= lo(t1) ^ hi(t2) ^ hi(t3) ^ lo(t2) ^ hi(t1) ^ lo(t3);  emit x
+// Streams are independent (no neighbour exchange).  64-bit shifts and XORs
+// become SHF/LOP3 pairs; the xor128 (period-4 register ring) and xorwow
+// (period-5 ring) recurrences are unrolled 20 rounds deep so the state never
+// moves between registers.  Integer-issue bound, not HBM bound.
+#include "device.cuh"
+#include "kernels.h"
+#include "sinks.cuh"
+
+namespace ciprng {
+
+__device__ __forceinline__ uint32_t fold6(uint64_t t1, uint64_t t2, uint64_t t3) {
+    return (uint32_t)t1 ^ (uint32_t)(t2 >> 32) ^ (uint32_t)(t3 >> 32) ^ (uint32_t)t2 ^ (uint32_t)(t1 >> 32) ^
+           (uint32_t)t3;
+}
+
+template <class Sink>
+__global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
+    Sink sink(a);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t n_tiles = (a.s_count + 31) / 32;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *P = a.state;
+    const uint64_t L = a.n_local;
+
+    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
+         tile += warps) {
+        const uint64_t row = tile * 32 + lane;
+        const bool valid = row < a.s_count;
+        const uint64_t s = a.s_begin + row;
+        uint64_t ra = 0, rb[4] = {0, 0, 0, 0}, rc[5] = {0, 0, 0, 0, 0}, rd = 0;
+        uint32_t x = 0;
+        auto ld64 = [&](int k) -> uint64_t {
+            return (uint64_t)P[(2 * k) * L + s] | ((uint64_t)P[(2 * k + 1) * L + s] << 32);
+        };
+        if (valid) {
+            ra = ld64(0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rb[k] = ld64(1 + k);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) rc[k] = ld64(5 + k);
+            rd = ld64(10);
+            x = P[22 * L + s];
+        }
+        sink.begin_tile();
+        uint64_t i = 0;
+        for (; i + 20 <= a.n; i += 20) {
+            uint32_t o[4];
+#pragma unroll
+            for (int k = 0; k < 20; ++k) {
+                ra = xor64_step(ra);
+                rb[k % 4] = xor128_f64(rb[k % 4], rb[(k + 3) % 4]);
+                rc[k % 5] = xorwow_f64(rc[k % 5], rc[(k + 4) % 5]);
+                rd += 362437u;
+                x ^= fold6(ra, rb[k % 4], rd + rc[k % 5]);
+                o[k % 4] = x;
+                if (k % 4 == 3) sink.put4(row, i + k - 3, o[0], o[1], o[2], o[3], valid);
+            }
+        }
+        // tail (fewer than 20 rounds): same recurrences with register moves
+        auto step = [&]() -> uint32_t {
+            ra = xor64_step(ra);
+            uint64_t nb = xor128_f64(rb[0], rb[3]);
+            rb[0] = rb[1]; rb[1] = rb[2]; rb[2] = rb[3]; rb[3] = nb;
+            uint64_t nc = xorwow_f64(rc[0], rc[4]);
+            rc[0] = rc[1]; rc[1] = rc[2]; rc[2] = rc[3]; rc[3] = rc[4]; rc[4] = nc;
+            rd += 362437u;
+            x ^= fold6(ra, nb, rd + nc);
+            return x;
+        };
+        for (; i + 4 <= a.n; i += 4) {
+            uint32_t o0 = step(), o1 = step(), o2 = step(), o3 = step();
+            sink.put4(row, i, o0, o1, o2, o3, valid);
+        }
+        for (; i < a.n; ++i) sink.put1(row, i, step(), valid);
+        if (valid) {
+            auto st64 = [&](int k, uint64_t v) {
+                P[(2 * k) * L + s] = (uint32_t)v;
+                P[(2 * k + 1) * L + s] = (uint32_t)(v >> 32);
+            };
+            st64(0, ra);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) st64(1 + k, rb[k]);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) st64(5 + k, rc[k]);
+            st64(10, rd);
+            P[22 * L + s] = x;
+        }
+    }
+    sink.finish(a);
+}
+
+int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+    if (a.s_count == 0) return 0;
+    const uint64_t tiles = (a.s_count + 31) / 32;
+    const int wpb = 8;
+    uint64_t blocks = (tiles + wpb - 1) / wpb;
+    if (mode == 2) {
+        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
+        v0_kernel<StatsSink><<<(int)blocks, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a);
+    } else {
+        v0_kernel<StoreSink><<<(int)blocks, 32 * wpb, 0, st>>>(a);
+    }
+    return 1;
+}
+
+}  // namespace ciprng

@@ -1,0 +1,124 @@
+// gen_v2.cu -- V2: Alg. 5 BBS kernel on sm_100a.
+//
+// Per stream: 8 BBS instances (y_j, modulus index m_j) with M_j < 2^16
+// (Q13), x and the shared cell tp.  Per call: the arrangement
+// arrays are chosen from the call-entry states of bbs1 and bbs2:
+//   o1 = array_comb[bbs1 & 7], o2 = array_comb[8 + (bbs2 & 7)]  (Q15, Q16)
+// Per round:
+//   8 x { y_j = y_j^2 mod M_j;  t = (t << 4) | (y_j & 15) }
+//   shift = sq(bbs3) & 3;  t <<= shift;  t |= sq(bbs1) & array_shift[shift]
+//   shift = sq(bbs7) & 3;  t <<= shift;  t |= sq(bbs2) & array_shift[shift]
+//   t ^= tp[o1] ^ tp[o2];  tp = t;  x ^= t;  emit x
+// with array_shift[s] = {0,1,3,7}[s] = (1 << s) - 1 (Q17, Q18).
+// At the end of a call with n > 0 the (y, m) pairs rotate: instance j is
+// stored in place j+1, instance 8 in place 1 (Q19, Q20).
+//
+// The modulus is division-free (Barrett with mu = floor(2^32 / M), one
+// conditional subtraction; device.cuh).  The neighbour exchange is two
+// data-dependent SHFL.IDX per number.  12 squarings (~5 integer ops each)
+// per number: integer-issue bound.
+#include "device.cuh"
+#include "kernels.h"
+#include "sinks.cuh"
+
+namespace ciprng {
+
+struct Bbs8 {
+    uint32_t y[8], M[8], mu[8];
+};
+
+__device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        b.y[j] = barrett_sq(b.y[j], b.M[j], b.mu[j]);
+        t = (t << 4) | (b.y[j] & 15u);
+    }
+    uint32_t sh;
+    b.y[2] = barrett_sq(b.y[2], b.M[2], b.mu[2]);
+    sh = b.y[2] & 3u;
+    t <<= sh;
+    b.y[0] = barrett_sq(b.y[0], b.M[0], b.mu[0]);
+    t |= b.y[0] & ((1u << sh) - 1u);
+    b.y[6] = barrett_sq(b.y[6], b.M[6], b.mu[6]);
+    sh = b.y[6] & 3u;
+    t <<= sh;
+    b.y[1] = barrett_sq(b.y[1], b.M[1], b.mu[1]);
+    t |= b.y[1] & ((1u << sh) - 1u);
+    return t;
+}
+
+template <class Sink>
+__global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
+    Sink sink(a);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t C = a.C;
+    const uint32_t off = lane % C, gbase = lane - off;
+    const uint64_t n_tiles = (a.s_count + 31) / 32;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *P = a.state;
+    const uint64_t L = a.n_local;
+
+    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
+         tile += warps) {
+        const uint64_t row = tile * 32 + lane;
+        const bool valid = row < a.s_count;
+        const uint64_t s = a.s_begin + row;
+        Bbs8 b;
+        uint32_t m[8];
+        uint32_t x = 0, tp = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            b.y[j] = valid ? P[j * L + s] : 2u;
+            m[j] = valid ? P[(8 + j) * L + s] : 0u;
+            b.M[j] = __ldg(a.mod + 2 * m[j]);
+            b.mu[j] = __ldg(a.mod + 2 * m[j] + 1);
+        }
+        if (valid) {
+            x = P[16 * L + s];
+            tp = P[17 * L + s];
+        }
+        const uint32_t src1 = gbase + a.comb.t[b.y[0] & 7u][off];
+        const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
+        sink.begin_tile();
+        auto round = [&]() -> uint32_t {
+            uint32_t t = v2_strategy(b);
+            t ^= __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
+            tp = t;
+            x ^= t;
+            return x;
+        };
+        uint64_t i = 0;
+        for (; i + 4 <= a.n; i += 4) {
+            uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
+            sink.put4(row, i, o0, o1, o2, o3, valid);
+        }
+        for (; i < a.n; ++i) sink.put1(row, i, round(), valid);
+        if (valid && a.n > 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                P[((j + 1) & 7) * L + s] = b.y[j];
+                P[(8 + ((j + 1) & 7)) * L + s] = m[j];
+            }
+            P[16 * L + s] = x;
+            P[17 * L + s] = tp;
+        }
+    }
+    sink.finish(a);
+}
+
+int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+    if (a.s_count == 0) return 0;
+    const uint64_t tiles = (a.s_count + 31) / 32;
+    const int wpb = 8;
+    uint64_t blocks = (tiles + wpb - 1) / wpb;
+    if (mode == 2) {
+        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
+        v2_kernel<StatsSink><<<(int)blocks, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a);
+    } else {
+        v2_kernel<StoreSink><<<(int)blocks, 32 * wpb, 0, st>>>(a);
+    }
+    return 1;
+}
+
+}  // namespace ciprng

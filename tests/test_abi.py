@@ -1,0 +1,89 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every
+entry point include/ciprng.h declares, rejects bad configurations before
+touching the device, and its division-free BBS squaring is exact."""
+import ctypes
+import subprocess
+
+import pytest
+
+import paper_1112_5239_b200 as P
+from paper_1112_5239_b200 import _lib
+
+
+def test_library_loads_and_exports_declared_symbols():
+    L = P.lib()
+    declared = P.declared_symbols()
+    assert len(declared) >= 14
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
+    for name in declared:
+        assert name in exported, name
+        assert getattr(L, name) is not None
+
+
+def test_version_string():
+    assert b"sm_100a" in P.lib().prng_version()
+
+
+def test_strerror_covers_all_statuses():
+    for st in range(0, -7, -1):
+        assert P.lib().prng_strerror(st) != b"unknown status"
+
+
+def test_barrett_modsq_exhaustive():
+    """Every modulus of the table, every y < M: barrett_sq == y*y % M."""
+    bad = ctypes.c_uint64(123)
+    assert P.lib().prng_selftest_modsq(ctypes.byref(bad)) == 0
+    assert bad.value == 0
+
+
+def _create(seed, first, n_local, variant, comb_size=0, comb=None, paper_defaults=0, store_path=0):
+    keep = None
+    if comb is not None:
+        keep = (ctypes.c_uint8 * len(comb))(*comb)
+    cfg = _lib.PrngConfig(comb_size=comb_size, comb=ctypes.cast(keep, ctypes.c_void_p) if keep else None,
+                          paper_defaults=paper_defaults, store_path=store_path)
+    h = ctypes.c_void_p()
+    rc = P.lib().prng_create_shard(seed, first, n_local, variant, ctypes.byref(cfg), ctypes.byref(h))
+    if rc == 0:
+        P.lib().prng_destroy(h)
+    return rc
+
+
+@pytest.mark.parametrize(
+    "args",
+    [
+        dict(seed=0, first=0, n_local=32, variant=3),                     # unknown variant
+        dict(seed=0, first=0, n_local=0, variant=1),                      # no streams
+        dict(seed=0, first=0, n_local=33, variant=1),                     # incomplete group
+        dict(seed=0, first=16, n_local=32, variant=1),                    # misaligned shard
+        dict(seed=0, first=0, n_local=4, variant=1, comb_size=3, comb=[0, 1, 2, 0, 1, 2]),  # C not 2^k
+        dict(seed=0, first=0, n_local=4, variant=1, comb_size=4),         # defaults need C = 32
+        dict(seed=0, first=0, n_local=4, variant=1, comb_size=4, comb=[0, 1, 2, 4, 0, 1, 2, 3]),  # entry >= C
+        dict(seed=0, first=0, n_local=2, variant=0, paper_defaults=1),    # Q26
+        dict(seed=0, first=0, n_local=32, variant=1, paper_defaults=1),
+        dict(seed=0, first=0, n_local=32, variant=1, store_path=7),
+    ],
+)
+def test_create_rejects_bad_config_without_device(args):
+    assert _create(**args) == _lib.PRNG_EINVAL
+
+
+def test_null_pointers_rejected():
+    L = P.lib()
+    assert L.prng_create(0, 32, 1, None) == _lib.PRNG_EINVAL
+    assert L.prng_generate(None, 4, None, None) == _lib.PRNG_EINVAL
+    assert L.prng_consume(None, 4, None, None) == _lib.PRNG_EINVAL
+    assert L.prng_destroy(None) == 0
+
+
+def test_sass_has_no_tensor_core_and_has_tma_store():
+    """The V1 fast store kernel's tile path is a TMA bulk tensor store
+    (UTMASTG / UBLKCP), and nothing here is a dense contraction (no UTC*MMA)."""
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    sass = r.stdout
+    assert "UTMASTG" in sass or "UBLKCP" in sass
+    assert "UTCHMMA" not in sass and "HMMA" not in sass
+    assert "SHFL.IDX" in sass

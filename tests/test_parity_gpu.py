@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle, word
+for word (bit-exact: the method is integer-only, so exactly one output is
+correct under the DESIGN.md readings).  Sizes span several warps/tiles and a
+ragged tail; edge cases: n = 0, n not a multiple of 4, incomplete last tile,
+custom combination arrays, multi-call state carry, V2 per-call selection and
+rotation, shards, host-buffer path, misaligned outputs."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1112_5239_b200 as P
+import workloads as W
+from tests.gpu_helpers import first_mismatch, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+SEEDS = W.SEEDS
+NS = [0, 1, 3, 4, 5, 127, 128, 1000]
+
+
+def _check(variant, seed, S, ns, **kw):
+    comb_size = kw.pop("comb_size", None)
+    comb = kw.pop("comb", None)
+    store_path = kw.pop("store_path", P.STORE_AUTO)
+    first = kw.pop("first", 0)
+    paper_defaults = kw.pop("paper_defaults", False)
+    outs, planes, info = gpu_run(variant, seed, S, ns, first=first, comb_size=comb_size, comb=comb,
+                                 paper_defaults=paper_defaults, store_path=store_path, **kw)
+    ro, rplanes = oracle_run(variant, seed, S, ns, first=first, comb_size=comb_size or 32, comb=comb,
+                             paper_defaults=paper_defaults)
+    for k, (a, b) in enumerate(zip(outs, ro)):
+        assert np.array_equal(a, b), f"call {k} (n={ns[k]}): {first_mismatch(a, b)}"
+    assert np.array_equal(planes, rplanes), f"state: {first_mismatch(planes, rplanes)}"
+    return info
+
+
+# ------------------------------------------------------------------------ V1
+@pytest.mark.parametrize("seed", SEEDS)
+@pytest.mark.parametrize("S", [32, 64, 96, 1024, 16384])
+@pytest.mark.parametrize("store_path", [P.STORE_DIRECT, P.STORE_TMA])
+def test_v1_default_tables(seed, S, store_path):
+    info = _check(W.V1, seed, S, NS, store_path=store_path)
+    assert info.kernel_launches == 1
+
+
+@pytest.mark.parametrize("C", [1, 2, 4, 8, 32])
+def test_v1_custom_tables(C):
+    gen = W.rng(100 + C)
+    comb = W.random_comb(gen, C, 2)
+    for S in (C * 3 if C < 32 else 64, 1024):
+        _check(W.V1, SEEDS[0], S, [5, 128, 3], comb_size=C, comb=comb)
+
+
+def test_v1_spec_tiny_tables():
+    """T=4, c=2, comb1=[0,1], comb2=[1,0]."""
+    _check(W.V1, 12345, 4, [1, 2, 7], comb_size=2, comb=np.array([0, 1, 1, 0], np.uint8))
+
+
+def test_v1_shard_equals_slice():
+    S = 2048
+    whole, _, _ = gpu_run(W.V1, SEEDS[0], S, [64])
+    lo, _, _ = gpu_run(W.V1, SEEDS[0], S // 2, [64], first=0)
+    hi, _, _ = gpu_run(W.V1, SEEDS[0], S // 2, [64], first=S // 2)
+    assert np.array_equal(np.concatenate([lo[0], hi[0]]), whole[0])
+
+
+def test_v1_split_invariance_gpu():
+    a, _, _ = gpu_run(W.V1, 7, 256, [100])
+    b, _, _ = gpu_run(W.V1, 7, 256, [36, 64])
+    assert np.array_equal(a[0], np.concatenate(b, axis=1))
+
+
+def test_v1_misaligned_output_falls_back():
+    """Output pointer 4 bytes off 16-byte alignment: AUTO/DIRECT fall back to
+    scalar stores and stay exact; explicit TMA reports PRNG_EALIGN."""
+    _check(W.V1, 3, 128, [8, 12], out_offset_words=1)
+    _check(W.V1, 3, 128, [8], out_offset_words=1, store_path=P.STORE_DIRECT)
+    with pytest.raises(P.PrngError) as ei:
+        gpu_run(W.V1, 3, 128, [8], out_offset_words=1, store_path=P.STORE_TMA)
+    assert ei.value.status == -4
+
+
+def test_v1_generate_host_matches_device():
+    g1 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
+    g2 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
+    for n in (128, 36):
+        dev = P.as_u32(g1.generate(n))
+        host = g2.generate_host(n).numpy().view(np.uint32)
+        assert np.array_equal(dev, host)
+
+
+def test_v1_set_state_resume():
+    """Checkpoint/resume (the written-back state is a checkpoint)."""
+    g = P.ChaoticPRNG(5, 256, W.V1)
+    g.generate(17)
+    ckpt = g.get_state()
+    a = P.as_u32(g.generate(40))
+    g.set_state(ckpt)
+    b = P.as_u32(g.generate(40))
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------------ V0
+@pytest.mark.parametrize("seed", SEEDS)
+@pytest.mark.parametrize("S", [1, 31, 32, 33, 1000])
+def test_v0(seed, S):
+    _check(W.V0, seed, S, [0, 1, 3, 4, 19, 20, 21, 100, 5])
+
+
+def test_v0_paper_defaults_c1_full():
+    """BASELINE configs[0]: 1 stream, Listing 1 defaults, 10^6 outputs."""
+    _check(W.V0, 0, 1, [10**6], paper_defaults=True)
+
+
+# ------------------------------------------------------------------------ V2
+@pytest.mark.parametrize("seed", SEEDS)
+@pytest.mark.parametrize("S", [32, 64, 96, 1024])
+def test_v2_default_tables(seed, S):
+    _check(W.V2, seed, S, [0, 1, 3, 4, 5, 64, 7])
+
+
+@pytest.mark.parametrize("C", [1, 2, 4, 32])
+def test_v2_custom_tables(C):
+    gen = W.rng(200 + C)
+    comb = W.random_comb(gen, C, 16)
+    _check(W.V2, SEEDS[1], 96 if C < 32 else 128, [5, 64, 3], comb_size=C, comb=comb)
+
+
+def test_v2_hand_trace_injected(golden):
+    """The hand-traced C=1 trace (tests/golden) through the GPU via set_state."""
+    e = golden["hand_traces"]["v2_c1_trace"]
+    midx = O.moduli().index(e["M"])
+    g = P.ChaoticPRNG(0, 1, W.V2, comb_size=1, comb=np.zeros(16, np.uint8))
+    planes = np.array([[v] for v in e["y"] + [midx] * 8 + [e["x"], e["tp"]]], dtype=np.uint32)
+    g.set_state(planes)
+    out = P.as_u32(g.generate(2))[0].tolist()
+    assert out == e["outputs"]
+    assert g.get_state()[:8, 0].tolist() == e["y_after_call"]
+
+
+def test_v1_hand_trace_injected(golden):
+    e = golden["hand_traces"]["v1_c2_trace"]
+    g = P.ChaoticPRNG(0, 2, W.V1, comb_size=2, comb=np.array(e["comb1"] + e["comb2"], np.uint8))
+    planes = np.array([[ln["xor128"][k] for ln in e["lanes"]] for k in range(4)]
+                      + [[ln["x"] for ln in e["lanes"]], [ln["tp"] for ln in e["lanes"]]], dtype=np.uint32)
+    g.set_state(planes)
+    assert P.as_u32(g.generate(3)).tolist() == e["outputs"]
+
+
+# ------------------------------------------------------------------ consumer
+@pytest.mark.parametrize("variant,S,n", [(W.V0, 100, 38), (W.V1, 2048, 130), (W.V1, 96, 6), (W.V2, 1024, 66)])
+def test_consume_matches_oracle_stats(variant, S, n):
+    g = P.ChaoticPRNG(SEEDS[0], S, variant)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        g.consume(n, stats)
+    got = P.as_u64(stats)
+    st = O.init_states(variant, SEEDS[0], 0, S)
+    ref = np.zeros(258, np.uint64)
+    for _ in range(2):
+        O.stats(O.generate(variant, st, n), ref)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    # consume advances the state exactly like generate
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+
+
+def test_consume_custom_tables_and_odd_n():
+    comb = W.random_comb(W.rng(9), 4, 2)
+    g = P.ChaoticPRNG(1, 64, W.V1, comb_size=4, comb=comb)
+    stats = g.consume(10)
+    st = O.init_states(W.V1, 1, 0, 64)
+    ref = O.stats(O.generate(W.V1, st, 10, comb_size=4, comb=comb))
+    assert np.array_equal(P.as_u64(stats), ref)
+    with pytest.raises(P.PrngError):
+        g.consume(3)
+
+
+# -------------------------------------------------------------------- digest
+def test_digest_matches_oracle():
+    g = P.ChaoticPRNG(SEEDS[0], 512, W.V1, shard=(256, 256))
+    out = g.generate(33)
+    d = int(P.as_u64(P.digest(out, first_stream=256))[0])
+    assert d == O.digest(P.as_u32(out), 256)
+
+
+# ------------------------------------------------------------- full configs
+@pytest.mark.slow
+def test_c2_full_size_two_calls():
+    """BASELINE configs[1]: V1, 2^20 streams x 128, default tables, the exact
+    launch configuration bench.py times (store path AUTO)."""
+    S, n = 2**20, 128
+    g = P.ChaoticPRNG(SEEDS[0], S, W.V1)
+    st = O.init_states(W.V1, SEEDS[0], 0, S)
+    for _ in range(2):
+        a = P.as_u32(g.generate(n))
+        b = O.generate(W.V1, st, n)
+        assert np.array_equal(a, b), first_mismatch(a, b)
+    assert np.array_equal(g.get_state(), O.state_planes(W.V1, st))
+
+
+@pytest.mark.slow
+def test_c3_full_size_two_calls():
+    """BASELINE configs[2]: V2, 2^20 streams x 64."""
+    S, n = 2**20, 64
+    g = P.ChaoticPRNG(SEEDS[0], S, W.V2)
+    st = O.init_states(W.V2, SEEDS[0], 0, S)
+    for _ in range(2):
+        a = P.as_u32(g.generate(n))
+        b = O.generate(W.V2, st, n)
+        assert np.array_equal(a, b), first_mismatch(a, b)
+    assert np.array_equal(g.get_state(), O.state_planes(W.V2, st))
+
+
+@pytest.mark.slow
+def test_c4_shape_sampled_groups():
+    """BASELINE configs[3] shape (2^23 streams x 256 per call): 3 calls on the
+    GPU, 64 sampled 32-stream groups replayed by the oracle from their own
+    shard seeds (per-stream seeding makes each group independent)."""
+    S, n, calls = 2**23, 256, 3
+    g = P.ChaoticPRNG(SEEDS[0], S, W.V1)
+    gen = W.rng(44)
+    groups = np.sort(gen.choice(S // 32, 64, replace=False))
+    rows = (groups[:, None] * 32 + np.arange(32)[None, :]).ravel()
+    sts = [O.init_states(W.V1, SEEDS[0], int(gr) * 32, 32) for gr in groups]
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+        sampled = P.as_u32(out[torch.as_tensor(rows, device="cuda")])
+        ref = np.concatenate([O.generate(W.V1, st, n) for st in sts])
+        assert np.array_equal(sampled, ref), first_mismatch(sampled, ref)
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_gpu_output_statistics():
+    from tests import statcheck
+
+    for variant in (W.V0, W.V1, W.V2):
+        g = P.ChaoticPRNG(SEEDS[0], 2**14, variant)
+        out = P.as_u32(g.generate(256))
+        assert statcheck.passes(statcheck.battery(out)), variant
+        s = P.as_u64(g.consume(1024))
+        assert abs(statcheck.pi_zscore(int(s[0]), int(s[1]))) < 5
+        assert 1e-4 < statcheck.hist_chi2_p(s[2:]) < 1 - 1e-4

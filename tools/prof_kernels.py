@@ -1,0 +1,40 @@
+"""Small driver for ncu captures: a few calls of one workload through the
+C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|consume} [calls]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1112_5239_b200 as P  # noqa: E402
+import workloads as W  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "v1"
+calls = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+seed = W.SEEDS[0]
+if which in ("v1", "v1direct"):
+    S, n = 2**20, 128
+    g = P.ChaoticPRNG(seed, S, P.V1, store_path=P.STORE_DIRECT if which == "v1direct" else P.STORE_TMA)
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+elif which == "v2":
+    S, n = 2**20, 64
+    g = P.ChaoticPRNG(seed, S, P.V2)
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+elif which == "v0":
+    S, n = 2**20, 128
+    g = P.ChaoticPRNG(seed, S, P.V0)
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+elif which == "consume":
+    S, n = 2**20, 1024
+    g = P.ChaoticPRNG(seed, S, P.V1)
+    st = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    for _ in range(calls):
+        g.consume(n, st)
+torch.cuda.synchronize()
+print("done", which)
