@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
                 xA ^= gA ^ nb;
                 xB ^= gB ^ nb;
                 u = gA ^ gB;
-                sink.put1(rA, i, xA, valid);
-                sink.put1(rB, i, xB, valid);
+                sink.put1(rA, i, xA, valid, 0);
+                sink.put1(rB, i, xB, valid, 1);
             }
         }
 #undef CIPRNG_V1_ROUND

@@ -30,7 +30,7 @@ struct StoreSink {
             p[3] = o3;
         }
     }
-    __device__ __forceinline__ void put1(uint64_t row, uint64_t i, uint32_t o, bool valid) {
+    __device__ __forceinline__ void put1(uint64_t row, uint64_t i, uint32_t o, bool valid, int = 0) {
         if (valid) out[row * n + i] = o;
     }
     __device__ __forceinline__ void finish(const GenArgs &) {}
@@ -46,11 +46,11 @@ struct StatsSink {
     uint32_t *hist;      // this warp's 256 bins
     uint64_t inside;     // this lane's count
     uint32_t inside32;   // fast accumulator, folded into `inside`
-    uint32_t pend;       // stashed even-round value for put1 tails
+    uint32_t pend[2];    // stashed even-round value for put1 tails, per stream slot
     uint64_t pairs;      // valid pairs seen by this lane
     uint64_t n;
     __device__ __forceinline__ explicit StatsSink(const GenArgs &a)
-        : inside(0), inside32(0), pend(0), pairs(0), n(a.n) {
+        : inside(0), inside32(0), pend{0, 0}, pairs(0), n(a.n) {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
         for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
@@ -69,14 +69,15 @@ struct StatsSink {
         pairs += 2;
         if (inside32 >= 0x80000000u) { inside += inside32; inside32 = 0; }
     }
-    __device__ __forceinline__ void put1(uint64_t, uint64_t i, uint32_t o, bool valid) {
+    // slot: which of the lane's streams (the V1 fast kernel owns two)
+    __device__ __forceinline__ void put1(uint64_t, uint64_t i, uint32_t o, bool valid, int slot = 0) {
         if (!valid) return;
         atomicAdd(&hist[o >> 24], 1u);
         if (i & 1) {
-            inside32 += pi_inside(pend, o);
+            inside32 += pi_inside(pend[slot], o);
             pairs += 1;
         } else {
-            pend = o;
+            pend[slot] = o;
         }
     }
     __device__ void finish(const GenArgs &a) {
