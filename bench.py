@@ -200,7 +200,7 @@ def run_ours(args):
         torch.cuda.set_device(lr)
         dist = None
     dev = torch.device("cuda", lr)
-    S, n = S_PER_GPU, N_PER_STREAM
+    S, n = args.streams or S_PER_GPU, args.n or N_PER_STREAM
     g = P.ChaoticPRNG(W.SEEDS[0], S * ws, P.V1, shard=(rank * S, S), store_path=args.store_path)
     out = torch.empty((S, n), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
@@ -278,14 +278,15 @@ def run_ours(args):
         "dtype": "u32",
         "data": "synthetic (seeded; SplitMix64 per-stream seeding, seed 0x0123456789ABCDEF)",
         "config": {
-            "workload": "C2 (BASELINE configs[1]): V1 Alg.4 xor128 + neighbour combination (default C=32 arrays), "
+            "workload": ("C2 (BASELINE configs[1]): " if (S, n) == (S_PER_GPU, N_PER_STREAM) else "EXPERIMENT: ")
+                        + "V1 Alg.4 xor128 + neighbour combination (default C=32 arrays), "
                         f"{S} streams x {n} numbers per GPU per step, stored to HBM",
             "variant": "v1",
             "streams_per_gpu": S,
             "n_per_stream": n,
             "global_streams": S * ws,
             "store_path": {1: "direct", 2: "tma"}.get(store_path_used, str(store_path_used)),
-            "l2": "output 512 MiB per step per GPU > 126 MB L2 (inputs larger than L2, no flush)",
+            "l2": f"output {4 * S * n >> 20} MiB per step per GPU > 126 MB L2 (inputs larger than L2, no flush)",
             "parallelism": f"stream-sharded x{ws} (no collective on the store path)",
         },
         "roofline": {
@@ -374,6 +375,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--streams", type=int, default=0, help="experiment override of streams per GPU")
+    ap.add_argument("--n", type=int, default=0, help="experiment override of numbers per stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

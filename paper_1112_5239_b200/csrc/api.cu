@@ -100,6 +100,7 @@ struct prng_s {
     uint32_t n_mod = 0;
     int num_sms = 148;
     int persistent_blocks = 0;
+    V1Tuning v1tune;
     // last call info
     int last_path = 0;
     uint32_t last_launches = 0;
@@ -107,6 +108,7 @@ struct prng_s {
     struct TmEntry {
         const void *ptr = nullptr;
         uint64_t n = 0, rows = 0;
+        int cols = 0;
         CUtensorMap map;
         bool ok = false;
     } tm[4];
@@ -120,21 +122,42 @@ struct prng_s {
 
 namespace {
 
-const CUtensorMap *tensor_map(prng_t *h, const uint32_t *out, uint64_t n, uint64_t rows) {
+const CUtensorMap *tensor_map(prng_t *h, const uint32_t *out, uint64_t n, uint64_t rows, int cols) {
     for (auto &e : h->tm)
-        if (e.ok && e.ptr == out && e.n == n && e.rows == rows) return &e.map;
+        if (e.ok && e.ptr == out && e.n == n && e.rows == rows && e.cols == cols) return &e.map;
     EncodeTiledFn fn = encode_fn();
     if (!fn) return nullptr;
     auto &e = h->tm[h->tm_next];
     h->tm_next = (h->tm_next + 1) & 3;
     cuuint64_t gdim[2] = {n, rows};
     cuuint64_t gstride[1] = {n * 4};
-    cuuint32_t box[2] = {16, 64};
+    if (cols >= 64) {
+        // 3-D band view {32 words, rows, n/32 bands}; box {32, 64, cols/32}
+        cuuint64_t gdim3[3] = {32, rows, n / 32};
+        cuuint64_t gstride3[2] = {n * 4, 128};
+        cuuint32_t box3[3] = {32, 64, (cuuint32_t)(cols / 32)};
+        cuuint32_t estr3[3] = {1, 1, 1};
+        CUresult r3 = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t *>(out), gdim3, gstride3,
+                         box3, estr3, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        e.ok = (r3 == CUDA_SUCCESS);
+        e.cols = cols;
+        e.ptr = out;
+        e.n = n;
+        e.rows = rows;
+        return e.ok ? &e.map : nullptr;
+    }
+    // box = cols rounds x 64 streams; swizzle span = the box row (cols * 4 B)
+    cuuint32_t box[2] = {(cuuint32_t)cols, 64};
     cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = cols == 8 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                  : cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                               : CU_TENSOR_MAP_SWIZZLE_64B;
     CUresult r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t *>(out), gdim, gstride, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     e.ok = (r == CUDA_SUCCESS);
+    e.cols = cols;
     e.ptr = out;
     e.n = n;
     e.rows = rows;
@@ -166,18 +189,20 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
         const bool fast = h->default_tables && h->C == 32;
         int kmode = mode;
         const CUtensorMap *tm = nullptr;
+        V1Tuning tune = h->v1tune;
+        if (tune.cols >= 64 && n % 32 != 0) tune.cols = 32;  // band boxes need whole 32-round bands
         if (mode == 0 && fast) {
             const bool tma_ok = a.vec && n < (1ull << 31) && s_count < (1ull << 31);
             if (h->store_path == PRNG_STORE_TMA && reinterpret_cast<uintptr_t>(out) % 16 != 0) return PRNG_EALIGN;
             if (h->store_path != PRNG_STORE_DIRECT && tma_ok) {
-                tm = tensor_map(h, out, n, s_count);
+                tm = tensor_map(h, out, n, s_count, tune.cols);
                 if (tm) {
                     kmode = 1;
                     path = PRNG_STORE_TMA;
                 }
             }
         }
-        launches = launch_v1(a, fast, kmode, tm, st, h->persistent_blocks);
+        launches = launch_v1(a, fast, kmode, tm, st, h->persistent_blocks, tune);
     } else {
         launches = launch_v2(a, mode, st, h->persistent_blocks);
     }
@@ -255,6 +280,20 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
     h->persistent_blocks = h->num_sms * 8;
+    // experiment overrides of the V1 store kernel shape
+    if (const char *v = std::getenv("CIPRNG_V1_COLS")) {
+        int c = std::atoi(v);
+        if (c == 8 || c == 16 || c == 32 || c == 64 || c == 128) h->v1tune.cols = c;
+    }
+    if (const char *v = std::getenv("CIPRNG_V1_PERSIST")) h->v1tune.grid_mode = std::atoi(v);
+    if (const char *v = std::getenv("CIPRNG_V1_WPB")) {
+        int w = std::atoi(v);
+        if (w >= 1 && w <= 8) h->v1tune.wpb = w;
+    }
+    if (const char *v = std::getenv("CIPRNG_V1_GRID")) {
+        int b = std::atoi(v);
+        if (b > 0) h->v1tune.grid_blocks = b * h->num_sms;
+    }
     const size_t words = (size_t)kStateWords[variant] * n_local;
     e = cudaMalloc(&h->state, words * 4);
     if (e != cudaSuccess) {
@@ -459,7 +498,7 @@ int prng_selftest_modsq(uint64_t *mismatches) {
     for (size_t k = 0; k + 1 < tab.size(); k += 2) {
         const uint32_t M = tab[k], mu = tab[k + 1];
         for (uint32_t y = 0; y < M; ++y)
-            if (barrett_sq(y, M, mu) != (y * y) % M) ++bad;
+            if (barrett_sq(y, 0u - M, mu) != (y * y) % M) ++bad;
     }
     *mismatches = bad;
     return PRNG_OK;

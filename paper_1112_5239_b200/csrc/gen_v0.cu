@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             rd = ld64(10);
             x = P[22 * L + s];
         }
-        sink.begin_tile();
+        sink.begin_row(0, row);
         uint64_t i = 0;
         for (; i + 20 <= a.n; i += 20) {
             uint32_t o[4];
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
                 rd += 362437u;
                 x ^= fold6(ra, rb[k % 4], rd + rc[k % 5]);
                 o[k % 4] = x;
-                if (k % 4 == 3) sink.put4(row, i + k - 3, o[0], o[1], o[2], o[3], valid);
+                if (k % 4 == 3) sink.put4(0, i + k - 3, o[0], o[1], o[2], o[3], valid);
             }
         }
         // tail (fewer than 20 rounds): same recurrences with register moves
@@ -76,9 +76,9 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
         };
         for (; i + 4 <= a.n; i += 4) {
             uint32_t o0 = step(), o1 = step(), o2 = step(), o3 = step();
-            sink.put4(row, i, o0, o1, o2, o3, valid);
+            sink.put4(0, i, o0, o1, o2, o3, valid);
         }
-        for (; i < a.n; ++i) sink.put1(row, i, step(), valid);
+        for (; i < a.n; ++i) sink.put1(0, i, step(), valid);
         if (valid) {
             auto st64 = [&](int k, uint64_t v) {
                 P[(2 * k) * L + s] = (uint32_t)v;

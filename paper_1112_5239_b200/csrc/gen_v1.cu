@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
             g0 = P[0 * L + s]; g1 = P[1 * L + s]; g2 = P[2 * L + s]; g3 = P[3 * L + s];
             x = P[4 * L + s]; tp = P[5 * L + s];
         }
-        sink.begin_tile();
+        sink.begin_row(0, row);
         uint64_t i = 0;
         for (; i + 4 <= a.n; i += 4) {
             uint32_t t, o0, o1, o2, o3;
@@ -65,14 +65,14 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
             g3 = xor128_f(g3, g2);
             t = g3 ^ __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
             tp = t; x ^= t; o3 = x;
-            sink.put4(row, i, o0, o1, o2, o3, valid);
+            sink.put4(0, i, o0, o1, o2, o3, valid);
         }
         for (; i < a.n; ++i) {  // ragged tail: plain step with register moves
             uint32_t g = xor128_f(g0, g3);
             g0 = g1; g1 = g2; g2 = g3; g3 = g;
             uint32_t t = g ^ __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
             tp = t; x ^= t;
-            sink.put1(row, i, x, valid);
+            sink.put1(0, i, x, valid);
         }
         if (valid) {
             P[0 * L + s] = g0; P[1 * L + s] = g1; P[2 * L + s] = g2; P[3 * L + s] = g3;
@@ -86,17 +86,26 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
 // Tile = 64 streams (2 groups) per warp; lane L: half h = L >> 4 (group),
 // j = L & 15, owns rows rA = 32h + j and rB = rA + 16 of the tile.
 constexpr int kFastTileRows = 64;
-constexpr int kTmaCols = 16;                                   // rounds per TMA box
-constexpr int kTmaTileBytes = kFastTileRows * kTmaCols * 4;    // 4 KiB
-constexpr int kTmaWarpBytes = 2 * kTmaTileBytes;               // double buffer
 
-// byte offset of 16-byte chunk c (0..3) of row r (0..63) in a 64-byte-row
-// tile written with CU_TENSOR_MAP_SWIZZLE_64B (16-byte chunk index XOR
-// address bits [7:8]); conflict-free for 8 consecutive rows.
-__device__ __forceinline__ uint32_t swz64(uint32_t r, uint32_t c) { return r * 64u + ((c ^ ((r >> 1) & 3u)) << 4); }
+// Byte offset of 16-byte chunk c of row r in a tile of kCols u32 columns
+// (row pitch P = 4 kCols bytes) written with CU_TENSOR_MAP_SWIZZLE_{P}B:
+// the chunk index is XORed with address bits [7, 7 + log2(P/16)), i.e. with
+// (r * P / 128) mod (P / 16).  For every P this makes the 8 lanes of one
+// STS.128 phase (8 consecutive rows, same chunk) hit 8 distinct 16-byte
+// bank groups.
+template <int kCols>
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
+    constexpr uint32_t P = kCols * 4;
+    return r * P + ((c ^ ((r * P >> 7) & (P / 16 - 1))) << 4);
+}
 
-template <class Sink, bool kTma>
-__global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+// kCols == 0: direct stores through the Sink (StoreSink: 128-bit STG per
+// 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
+// TMA tile store of kCols rounds x 64 streams per box, double-buffered.
+template <class Sink, int kCols>
+__global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr bool kTma = kCols > 0;
+    constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t h = lane >> 4, j = lane & 15u;
@@ -112,9 +121,9 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         // swizzled TMA boxes need 1 KiB-aligned shared addresses
         const uint32_t base = (smem_u32(smem_dyn) + 1023u) & ~1023u;
-        wsmem = base + (threadIdx.x >> 5) * kTmaWarpBytes;
+        wsmem = base + (threadIdx.x >> 5) * (2 * kTileBytes);
     }
-    uint32_t tma_issued = 0;  // tiles issued by this warp (lane 0 tracks groups)
+    uint32_t tma_issued = 0;  // boxes issued by this warp
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += warps) {
@@ -130,7 +139,8 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
             b0 = P[0 * L + sB]; b1 = P[1 * L + sB]; b2 = P[2 * L + sB]; b3 = P[3 * L + sB];
             xB = P[4 * L + sB]; tpB = P[5 * L + sB];
         }
-        sink.begin_tile();
+        sink.begin_row(0, rA);
+        sink.begin_row(1, rB);
         uint32_t u = tpA ^ tpB;  // u[j] = tp[j] ^ tp[j+16]
         uint32_t nb = 0;
 
@@ -143,27 +153,31 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
     u = GA ^ GB;                                         \
     OA = xA;                                             \
     OB = xB;
+#define CIPRNG_V1_BLOCK4(Q)                                                   \
+    {                                                                         \
+        uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;                      \
+        CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)                             \
+        CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)                             \
+        CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)                             \
+        CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)                             \
+        st_shared_v4(buf + swz<kCols>(rA_t, (Q)), oA0, oA1, oA2, oA3);        \
+        st_shared_v4(buf + swz<kCols>(rB_t, (Q)), oB0, oB1, oB2, oB3);        \
+    }
 
         uint64_t i = 0;
         if constexpr (kTma) {
-            // rounds in boxes of kTmaCols; n % 4 == 0 guaranteed by the host
-            for (uint64_t i0 = 0; i0 < a.n; i0 += kTmaCols) {
-                const uint32_t buf = wsmem + (tma_issued & 1u) * kTmaTileBytes;
+            // boxes of kCols rounds; n % 4 == 0 guaranteed by the host
+            for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
+                const uint32_t buf = wsmem + (tma_issued & 1u) * kTileBytes;
                 if (tma_issued >= 2) {
                     if (lane == 0) bulk_wait_read<1>();
                     __syncwarp();
                 }
+                if (i0 + kCols <= a.n) {  // full box: no per-block bound checks
 #pragma unroll
-                for (uint32_t q = 0; q < kTmaCols / 4; ++q) {
-                    if (i0 + 4 * q < a.n) {
-                        uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
-                        CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)
-                        CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)
-                        CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)
-                        CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)
-                        st_shared_v4(buf + swz64(rA_t, q), oA0, oA1, oA2, oA3);
-                        st_shared_v4(buf + swz64(rB_t, q), oB0, oB1, oB2, oB3);
-                    }
+                    for (uint32_t q = 0; q < kCols / 4; ++q) CIPRNG_V1_BLOCK4(q)
+                } else {
+                    for (uint32_t q = 0; i0 + 4 * q < a.n; ++q) CIPRNG_V1_BLOCK4(q)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -181,8 +195,8 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
                 CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)
                 CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)
                 CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)
-                sink.put4(rA, i, oA0, oA1, oA2, oA3, valid);
-                sink.put4(rB, i, oB0, oB1, oB2, oB3, valid);
+                sink.put4(0, i, oA0, oA1, oA2, oA3, valid);
+                sink.put4(1, i, oB0, oB1, oB2, oB3, valid);
             }
             for (; i < a.n; ++i) {  // ragged tail
                 uint32_t gA = xor128_f(a0, a3), gB = xor128_f(b0, b3);
@@ -192,15 +206,15 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
                 xA ^= gA ^ nb;
                 xB ^= gB ^ nb;
                 u = gA ^ gB;
-                sink.put1(rA, i, xA, valid, 0);
-                sink.put1(rB, i, xB, valid, 1);
+                sink.put1(0, i, xA, valid);
+                sink.put1(1, i, xB, valid);
             }
         }
+#undef CIPRNG_V1_BLOCK4
 #undef CIPRNG_V1_ROUND
         if (valid) {
             if (a.n > 0) {
-                // last round's t: t = g ^ nb; g is the newest ring entry (a3 after
-                // whole blocks; the tail shifts it into a3 as well)
+                // last round's t = g ^ nb; g is the newest ring entry, a3 / b3
                 tpA = a3 ^ nb;
                 tpB = b3 ^ nb;
             }
@@ -217,6 +231,123 @@ __global__ void __launch_bounds__(128) v1_fast_kernel(GenArgs a, const __grid_co
     sink.finish(a);
 }
 
+// ------------------------------------------------------------ band kernel
+// The HBM-friendly store path.  A warp owns a 64-stream tile; its output is
+// one contiguous slab of 64 rows x n words.  The tile is staged in shared
+// memory as kBands "bands" of 32 rounds (128 bytes) per row and written by
+// ONE 3-D TMA store per box: tensor map {32 words, rows (stride 4n bytes),
+// bands (stride 128 bytes)}, box {32, 64, kBands}, 128-byte swizzle.  With
+// kBands * 32 >= n a single bulk op writes the whole contiguous slab, so HBM
+// sees long contiguous runs instead of 128-byte pieces 4n bytes apart
+// (tools/pattern_bench: 7.16 TB/s vs 6.87 TB/s for 2-D 32-round boxes at
+// n = 128, 7.27 TB/s for a plain contiguous fill).  Requires n % 32 == 0.
+//
+// Persistent: each warp walks tiles tile, tile + W, ...; the state of its
+// next tile is prefetched into registers while the current one computes.
+template <int kBands, int kBufs>
+__global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr uint32_t kBoxRounds = 32 * kBands;
+    constexpr uint32_t kBoxBytes = 64 * kBoxRounds * 4;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t h = lane >> 4, j = lane & 15u;
+    const uint32_t src = (j + 1u) & 15u;
+    const uint64_t n_tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *P = a.state;
+    const uint64_t L = a.n_local;
+    const uint32_t rA_t = 32u * h + j, rB_t = rA_t + 16u;
+    // swizzled smem offsets of this lane's two rows (row r of a band lives at
+    // band*8192 + r*128, 16-byte chunk c at (c ^ (r & 7)) * 16)
+    const uint32_t offA = rA_t * 128u, offB = rB_t * 128u;
+    const uint32_t swA = rA_t & 7u, swB = rB_t & 7u;
+
+    extern __shared__ __align__(1024) uint8_t smem_dyn[];
+    const uint32_t wsmem = ((smem_u32(smem_dyn) + 1023u) & ~1023u) + (threadIdx.x >> 5) * (kBufs * kBoxBytes);
+    uint32_t issued = 0;
+
+    uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // prefetched state of `tile`
+    uint32_t pa[6] = {0, 0, 0, 0, 0, 0}, pb[6] = {0, 0, 0, 0, 0, 0};
+    auto prefetch = [&](uint64_t t) {
+        const uint64_t row0 = t * kFastTileRows;
+        if (t < n_tiles && row0 + 32u * h < a.s_count) {
+            const uint64_t sA = a.s_begin + row0 + rA_t, sB = sA + 16u;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                pa[k] = P[k * L + sA];
+                pb[k] = P[k * L + sB];
+            }
+        }
+    };
+    prefetch(tile);
+    for (; tile < n_tiles; tile += warps) {
+        const uint64_t row0 = tile * kFastTileRows;
+        const bool valid = row0 + 32u * h < a.s_count;
+        uint32_t a0 = pa[0], a1 = pa[1], a2 = pa[2], a3 = pa[3], xA = pa[4];
+        uint32_t b0 = pb[0], b1 = pb[1], b2 = pb[2], b3 = pb[3], xB = pb[4];
+        uint32_t u = pa[5] ^ pb[5];
+        uint32_t nb = 0;
+        prefetch(tile + warps);  // lands while this tile computes
+
+#define CIPRNG_V1_ROUND(GA, GA3, GB, GB3, OA, OB) \
+    GA = xor128_f(GA, GA3);                       \
+    GB = xor128_f(GB, GB3);                       \
+    nb = __shfl_sync(kFull, u, src, 16);          \
+    xA ^= GA ^ nb;                                \
+    xB ^= GB ^ nb;                                \
+    u = GA ^ GB;                                  \
+    OA = xA;                                      \
+    OB = xB;
+#define CIPRNG_V1_BLOCK4(Q)                                                                   \
+    {                                                                                         \
+        uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;                                      \
+        CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)                                             \
+        CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)                                             \
+        CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)                                             \
+        CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)                                             \
+        const uint32_t band = (Q) >> 3, c = (Q) & 7u;                                         \
+        st_shared_v4(buf + band * 8192u + offA + ((c ^ swA) << 4), oA0, oA1, oA2, oA3);       \
+        st_shared_v4(buf + band * 8192u + offB + ((c ^ swB) << 4), oB0, oB1, oB2, oB3);       \
+    }
+        for (uint64_t i0 = 0; i0 < a.n; i0 += kBoxRounds) {
+            const uint32_t buf = wsmem + (issued % kBufs) * kBoxBytes;
+            if (issued >= kBufs) {
+                if (lane == 0) bulk_wait_read<kBufs - 1>();
+                __syncwarp();
+            }
+            if (i0 + kBoxRounds <= a.n) {
+#pragma unroll 8
+                for (uint32_t q = 0; q < kBoxRounds / 4; ++q) CIPRNG_V1_BLOCK4(q)
+            } else {
+                for (uint32_t q = 0; i0 + 4 * q < a.n; ++q) CIPRNG_V1_BLOCK4(q)
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmap)),
+                    "r"(buf), "r"(0), "r"((int)row0), "r"((int)(i0 >> 5))
+                    : "memory");
+                bulk_commit();
+            }
+            ++issued;
+        }
+#undef CIPRNG_V1_BLOCK4
+#undef CIPRNG_V1_ROUND
+        if (valid) {
+            const uint64_t sA = a.s_begin + row0 + rA_t, sB = sA + 16u;
+            // n > 0 (the host never launches n == 0): last t = g ^ nb
+            P[0 * L + sA] = a0; P[1 * L + sA] = a1; P[2 * L + sA] = a2; P[3 * L + sA] = a3;
+            P[4 * L + sA] = xA; P[5 * L + sA] = a3 ^ nb;
+            P[0 * L + sB] = b0; P[1 * L + sB] = b1; P[2 * L + sB] = b2; P[3 * L + sB] = b3;
+            P[4 * L + sB] = xB; P[5 * L + sB] = b3 ^ nb;
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+}
+
 // ===================================================================== launch
 static int blocks_for(uint64_t warps_needed, int warps_per_block, int cap_blocks) {
     uint64_t b = (warps_needed + warps_per_block - 1) / warps_per_block;
@@ -225,25 +356,56 @@ static int blocks_for(uint64_t warps_needed, int warps_per_block, int cap_blocks
     return (int)b;
 }
 
+template <int kBands, int kBufs>
+static void launch_band(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles, int wpb, int grid_mode,
+                        cudaStream_t st) {
+    const size_t smem = (size_t)wpb * kBufs * 64 * 32 * kBands * 4 + 1024;  // + alignment slack
+    auto kern = v1_band_kernel<kBands, kBufs>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int grid = blocks_for(tiles, wpb, 0);
+    if (grid_mode != 0) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem);
+        if (grid_mode > 0 && grid_mode < per_sm) per_sm = grid_mode;
+        if (per_sm < 1) per_sm = 1;
+        grid = blocks_for(tiles, wpb, per_sm * sms);
+    }
+    kern<<<grid, 32 * wpb, smem, st>>>(a, tm);
+}
+
+template <int kCols>
+static void launch_fast_tma(const GenArgs &a, const CUtensorMap &tm, int grid, int wpb, cudaStream_t st) {
+    const size_t smem = (size_t)wpb * 2 * kFastTileRows * kCols * 4 + 1024;  // + alignment slack
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(v1_fast_kernel<StoreSink, kCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    v1_fast_kernel<StoreSink, kCols><<<grid, 32 * wpb, smem, st>>>(a, tm);
+}
+
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks) {
+              int persistent_blocks, const V1Tuning &tune) {
     // mode: 0 store-direct, 1 store-tma, 2 consume
     if (a.s_count == 0) return 0;
     if (fast) {
         const uint64_t tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
-        const int wpb = 4;
+        const int wpb = tune.wpb > 0 ? tune.wpb : 4;
+        const int cap = tune.grid_blocks > 0 ? tune.grid_blocks : 0;
         CUtensorMap dummy;
         if (tmap == nullptr) tmap = &dummy;
         if (mode == 0) {
-            int grid = blocks_for(tiles, wpb, 0);
-            v1_fast_kernel<StoreSink, false><<<grid, 32 * wpb, 0, st>>>(a, *tmap);
+            v1_fast_kernel<StoreSink, 0><<<blocks_for(tiles, wpb, cap), 32 * wpb, 0, st>>>(a, *tmap);
         } else if (mode == 1) {
-            int grid = blocks_for(tiles, wpb, 0);
-            size_t smem = (size_t)wpb * kTmaWarpBytes + 1024;  // + alignment slack
-            v1_fast_kernel<StoreSink, true><<<grid, 32 * wpb, smem, st>>>(a, *tmap);
+            const int grid = blocks_for(tiles, wpb, cap);
+            if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
+            else if (tune.cols == 128) launch_band<4, 1>(a, *tmap, tiles, wpb, tune.grid_mode, st);
+            else if (tune.cols == 8) launch_fast_tma<8>(a, *tmap, grid, wpb, st);
+            else if (tune.cols == 32) launch_fast_tma<32>(a, *tmap, grid, wpb, st);
+            else launch_fast_tma<16>(a, *tmap, grid, wpb, st);
         } else {
-            int grid = blocks_for(tiles, wpb, persistent_blocks);
-            v1_fast_kernel<StatsSink, false><<<grid, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a, *tmap);
+            int grid = blocks_for(tiles, 4, persistent_blocks);
+            v1_fast_kernel<StatsSink, 0><<<grid, 128, 4 * StatsSink::kSmemBytesPerWarp, st>>>(a, *tmap);
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;

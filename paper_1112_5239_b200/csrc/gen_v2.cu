@@ -24,26 +24,26 @@
 namespace ciprng {
 
 struct Bbs8 {
-    uint32_t y[8], M[8], mu[8];
+    uint32_t y[8], nM[8], mu[8];  // nM = 2^32 - M
 };
 
 __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
     uint32_t t = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        b.y[j] = barrett_sq(b.y[j], b.M[j], b.mu[j]);
+        b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
         t = (t << 4) | (b.y[j] & 15u);
     }
     uint32_t sh;
-    b.y[2] = barrett_sq(b.y[2], b.M[2], b.mu[2]);
+    b.y[2] = barrett_sq(b.y[2], b.nM[2], b.mu[2]);
     sh = b.y[2] & 3u;
     t <<= sh;
-    b.y[0] = barrett_sq(b.y[0], b.M[0], b.mu[0]);
+    b.y[0] = barrett_sq(b.y[0], b.nM[0], b.mu[0]);
     t |= b.y[0] & ((1u << sh) - 1u);
-    b.y[6] = barrett_sq(b.y[6], b.M[6], b.mu[6]);
+    b.y[6] = barrett_sq(b.y[6], b.nM[6], b.mu[6]);
     sh = b.y[6] & 3u;
     t <<= sh;
-    b.y[1] = barrett_sq(b.y[1], b.M[1], b.mu[1]);
+    b.y[1] = barrett_sq(b.y[1], b.nM[1], b.mu[1]);
     t |= b.y[1] & ((1u << sh) - 1u);
     return t;
 }
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         for (int j = 0; j < 8; ++j) {
             b.y[j] = valid ? P[j * L + s] : 2u;
             m[j] = valid ? P[(8 + j) * L + s] : 0u;
-            b.M[j] = __ldg(a.mod + 2 * m[j]);
+            b.nM[j] = 0u - __ldg(a.mod + 2 * m[j]);
             b.mu[j] = __ldg(a.mod + 2 * m[j] + 1);
         }
         if (valid) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         }
         const uint32_t src1 = gbase + a.comb.t[b.y[0] & 7u][off];
         const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
-        sink.begin_tile();
+        sink.begin_row(0, row);
         auto round = [&]() -> uint32_t {
             uint32_t t = v2_strategy(b);
             t ^= __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
@@ -91,9 +91,9 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         uint64_t i = 0;
         for (; i + 4 <= a.n; i += 4) {
             uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
-            sink.put4(row, i, o0, o1, o2, o3, valid);
+            sink.put4(0, i, o0, o1, o2, o3, valid);
         }
-        for (; i < a.n; ++i) sink.put1(row, i, round(), valid);
+        for (; i < a.n; ++i) sink.put1(0, i, round(), valid);
         if (valid && a.n > 0) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {

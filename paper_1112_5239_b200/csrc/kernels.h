@@ -20,11 +20,22 @@ struct InitArgs {
     uint32_t n_mod;
 };
 
+// Tuning of the V1 fast store kernel (defaults chosen from B200 measurements,
+// overridable for experiments with CIPRNG_V1_COLS / _WPB / _GRID).
+struct V1Tuning {
+    int cols = 32;        // TMA box width in rounds: 8, 16, 32 (2-D boxes) or
+                          // 64, 128 (3-D band boxes, needs n % 32 == 0)
+    int wpb = 2;          // warps per CTA
+    int grid_blocks = 0;  // 2-D kernels: 0 = one 64-stream tile per warp, > 0 = grid cap
+    int grid_mode = 0;    // band kernels: 0 = one tile per warp, -1 = persistent at
+                          // full occupancy, k > 0 = persistent with k CTAs per SM
+};
+
 // mode: 0 = store (direct), 1 = store (TMA tiles, V1 fast only), 2 = consume
 int launch_init(const InitArgs &a, cudaStream_t st);
 int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks);
+              int persistent_blocks, const V1Tuning &tune);
 int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);

@@ -15,12 +15,14 @@ struct StoreSink {
     uint32_t *out;
     uint64_t n;
     bool vec;
+    uint32_t *base[2];  // row start of each of the lane's (up to two) streams
     __device__ __forceinline__ explicit StoreSink(const GenArgs &a) : out(a.out), n(a.n), vec(a.vec != 0) {}
-    __device__ __forceinline__ void begin_tile() {}
-    __device__ __forceinline__ void put4(uint64_t row, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2,
+    // slot: which of the lane's streams (the V1 fast kernel owns two)
+    __device__ __forceinline__ void begin_row(int slot, uint64_t row) { base[slot] = out + row * n; }
+    __device__ __forceinline__ void put4(int slot, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2,
                                          uint32_t o3, bool valid) {
         if (!valid) return;
-        uint32_t *p = out + row * n + i;
+        uint32_t *p = base[slot] + i;
         if (vec) {
             st_v4(p, o0, o1, o2, o3);
         } else {
@@ -30,8 +32,8 @@ struct StoreSink {
             p[3] = o3;
         }
     }
-    __device__ __forceinline__ void put1(uint64_t row, uint64_t i, uint32_t o, bool valid, int = 0) {
-        if (valid) out[row * n + i] = o;
+    __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
+        if (valid) base[slot][i] = o;
     }
     __device__ __forceinline__ void finish(const GenArgs &) {}
     static constexpr int kSmemBytesPerWarp = 0;
@@ -57,8 +59,8 @@ struct StatsSink {
         __syncthreads();
         hist = all + 256u * (threadIdx.x >> 5);
     }
-    __device__ __forceinline__ void begin_tile() {}
-    __device__ __forceinline__ void put4(uint64_t, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
+    __device__ __forceinline__ void begin_row(int, uint64_t) {}
+    __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool valid) {
         if (!valid) return;
         atomicAdd(&hist[o0 >> 24], 1u);
@@ -69,8 +71,7 @@ struct StatsSink {
         pairs += 2;
         if (inside32 >= 0x80000000u) { inside += inside32; inside32 = 0; }
     }
-    // slot: which of the lane's streams (the V1 fast kernel owns two)
-    __device__ __forceinline__ void put1(uint64_t, uint64_t i, uint32_t o, bool valid, int slot = 0) {
+    __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
         if (!valid) return;
         atomicAdd(&hist[o >> 24], 1u);
         if (i & 1) {

@@ -243,3 +243,20 @@ def test_gpu_output_statistics():
         s = P.as_u64(g.consume(1024))
         assert abs(statcheck.pi_zscore(int(s[0]), int(s[1]))) < 5
         assert 1e-4 < statcheck.hist_chi2_p(s[2:]) < 1 - 1e-4
+
+
+@pytest.mark.parametrize("cols,wpb,grid,persist", [(8, 2, 0, 0), (32, 8, 0, 0), (16, 4, 1, 0), (32, 2, 3, 0),
+                                                   (8, 8, 1, 0), (64, 1, 0, 0), (64, 2, 0, -1), (128, 1, 0, 0),
+                                                   (128, 2, 0, -1), (128, 1, 0, 2)])
+def test_v1_store_kernel_shapes(monkeypatch, cols, wpb, grid, persist):
+    """Every V1 store-kernel shape (2-D TMA box width, 3-D band boxes,
+    warps per CTA, grid cap, persistent prefetching grid) is
+    bit-identical to the oracle, incl. partial boxes (n % box != 0), n not a
+    multiple of 32 (band modes fall back to 2-D boxes) and a half-empty last
+    tile (S % 64 == 32)."""
+    monkeypatch.setenv("CIPRNG_V1_COLS", str(cols))
+    monkeypatch.setenv("CIPRNG_V1_WPB", str(wpb))
+    monkeypatch.setenv("CIPRNG_V1_GRID", str(grid))
+    monkeypatch.setenv("CIPRNG_V1_PERSIST", str(persist))
+    for S in (96, 4096 + 32, 65536):
+        _check(W.V1, SEEDS[0], S, [4, 36, 128, 20, 96, 160, 256], store_path=P.STORE_TMA)
