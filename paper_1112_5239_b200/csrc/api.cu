@@ -87,6 +87,14 @@ constexpr int kStateWords[3] = {23, 6, 18};
 
 }  // namespace
 
+bool ciprng::pdl_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("CIPRNG_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 struct prng_s {
     int variant = 0;
     uint64_t seed = 0, first = 0, n_local = 0;

@@ -108,6 +108,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ------------------------------------------- programmatic dependent launch
+// Every kernel is launched with programmatic stream serialization (PDL): it
+// lets the next kernel on the stream be scheduled while this one drains, and
+// griddepcontrol.wait blocks until the previous grid has completed and its
+// memory is visible -- so nothing global is touched before pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // --------------------------------------------------- consumer statistics
 // Q24: pair (u, v) is "inside" iff u^2 + v^2 < 2^64 <=> v^2 <= ~(u^2).
 __device__ __forceinline__ uint32_t pi_inside(uint32_t u, uint32_t v) {
@@ -134,4 +142,45 @@ struct GenArgs {
     CombTables comb;
 };
 
+}  // namespace ciprng
+
+namespace ciprng {
+// ------------------------------------------ 64-bit xor-like on 32-bit halves
+// Listing 1's generators on (lo, hi) register pairs, written so that each
+// 64-bit constant shift is one funnel shift (ALU pipe) plus one plain 32-bit
+// shift expressed as a multiply (IMAD.SHL / IMAD.HI: FMA pipe).  Same values
+// as the uint64_t forms above; this only balances the two integer pipes.
+struct u64p {
+    uint32_t lo, hi;
+};
+__device__ __forceinline__ uint32_t shl32_fma(uint32_t v, int k) { return v * (1u << k); }
+__device__ __forceinline__ uint32_t shr32_fma(uint32_t v, int k) { return __umulhi(v, 1u << (32 - k)); }
+__device__ __forceinline__ u64p shl64(u64p a, int k) {  // a << k, 0 < k < 32
+    return {shl32_fma(a.lo, k), __funnelshift_l(a.lo, a.hi, k)};
+}
+__device__ __forceinline__ u64p shr64(u64p a, int k) {  // a >> k, 0 < k < 32
+    return {__funnelshift_r(a.lo, a.hi, k), shr32_fma(a.hi, k)};
+}
+__device__ __forceinline__ u64p xor64p(u64p a, u64p b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
+__device__ __forceinline__ u64p xor64p(u64p a, u64p b, u64p c) { return {a.lo ^ b.lo ^ c.lo, a.hi ^ b.hi ^ c.hi}; }
+__device__ __forceinline__ u64p xor64_step_p(u64p a) {
+    a = xor64p(a, shl64(a, 13));
+    a = xor64p(a, shr64(a, 7));
+    a = xor64p(a, shl64(a, 17));
+    return a;
+}
+__device__ __forceinline__ u64p xor128_f64p(u64p xk, u64p wk3) {
+    u64p t = xor64p(xk, shl64(xk, 11));
+    u64p r = xor64p(wk3, shr64(wk3, 19), t);
+    return xor64p(r, shr64(t, 8));
+}
+__device__ __forceinline__ u64p xorwow_f64p(u64p xk, u64p vk4) {
+    u64p t = xor64p(xk, shr64(xk, 2));
+    u64p r = xor64p(vk4, shl64(vk4, 4), t);
+    return xor64p(r, shl64(t, 1));
+}
+__device__ __forceinline__ u64p add64p(u64p a, u64p b) {
+    uint64_t s = ((uint64_t)a.hi << 32 | a.lo) + ((uint64_t)b.hi << 32 | b.lo);
+    return {(uint32_t)s, (uint32_t)(s >> 32)};
+}
 }  // namespace ciprng

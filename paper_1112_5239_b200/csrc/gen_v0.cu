@@ -23,6 +23,8 @@ __device__ __forceinline__ uint32_t fold6(uint64_t t1, uint64_t t2, uint64_t t3)
 template <class Sink>
 __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
     Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -51,17 +53,33 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
         sink.begin_row(0, row);
         uint64_t i = 0;
         for (; i + 20 <= a.n; i += 20) {
+            // unrolled on (lo, hi) halves: funnel shifts on the ALU pipe, plain
+            // shifts as multiplies on the FMA pipe (device.cuh, u64p)
+            u64p pa = {(uint32_t)ra, (uint32_t)(ra >> 32)}, pd = {(uint32_t)rd, (uint32_t)(rd >> 32)};
+            u64p pb[4], pc[5];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) pb[k] = {(uint32_t)rb[k], (uint32_t)(rb[k] >> 32)};
+#pragma unroll
+            for (int k = 0; k < 5; ++k) pc[k] = {(uint32_t)rc[k], (uint32_t)(rc[k] >> 32)};
+            const u64p weyl = {362437u, 0u};
             uint32_t o[4];
 #pragma unroll
             for (int k = 0; k < 20; ++k) {
-                ra = xor64_step(ra);
-                rb[k % 4] = xor128_f64(rb[k % 4], rb[(k + 3) % 4]);
-                rc[k % 5] = xorwow_f64(rc[k % 5], rc[(k + 4) % 5]);
-                rd += 362437u;
-                x ^= fold6(ra, rb[k % 4], rd + rc[k % 5]);
+                pa = xor64_step_p(pa);
+                pb[k % 4] = xor128_f64p(pb[k % 4], pb[(k + 3) % 4]);
+                pc[k % 5] = xorwow_f64p(pc[k % 5], pc[(k + 4) % 5]);
+                pd = add64p(pd, weyl);
+                const u64p t3 = add64p(pd, pc[k % 5]);
+                x ^= pa.lo ^ pb[k % 4].hi ^ t3.hi ^ pb[k % 4].lo ^ pa.hi ^ t3.lo;
                 o[k % 4] = x;
                 if (k % 4 == 3) sink.put4(0, i + k - 3, o[0], o[1], o[2], o[3], valid);
             }
+            ra = (uint64_t)pa.hi << 32 | pa.lo;
+            rd = (uint64_t)pd.hi << 32 | pd.lo;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rb[k] = (uint64_t)pb[k].hi << 32 | pb[k].lo;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) rc[k] = (uint64_t)pc[k].hi << 32 | pc[k].lo;
         }
         // tail (fewer than 20 rounds): same recurrences with register moves
         auto step = [&]() -> uint32_t {
@@ -103,9 +121,9 @@ int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
-        v0_kernel<StatsSink><<<(int)blocks, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a);
+        launch_k(v0_kernel<StatsSink>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
     } else {
-        v0_kernel<StoreSink><<<(int)blocks, 32 * wpb, 0, st>>>(a);
+        launch_k(v0_kernel<StoreSink>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }
     return 1;
 }

@@ -29,6 +29,8 @@ namespace ciprng {
 template <class Sink>
 __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
     Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t C = a.C;
     const uint32_t off = lane % C, gbase = lane - off;
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t h = lane >> 4, j = lane & 15u;
     const uint32_t src = (j + 1u) & 15u;  // width-16 shuffle source
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
         }
     }
     if constexpr (kTma) {
-        if (lane == 0) bulk_wait<0>();
+        if (lane == 0) bulk_wait_read<0>();  // smem must outlive the reads; global completion is ordered by the grid boundary
         __syncwarp();
     }
     sink.finish(a);
@@ -248,6 +252,8 @@ template <int kBands, int kBufs>
 __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr uint32_t kBoxRounds = 32 * kBands;
     constexpr uint32_t kBoxBytes = 64 * kBoxRounds * 4;
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t h = lane >> 4, j = lane & 15u;
     const uint32_t src = (j + 1u) & 15u;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_co
             P[4 * L + sB] = xB; P[5 * L + sB] = b3 ^ nb;
         }
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait_read<0>();  // smem must outlive the reads; global completion is ordered by the grid boundary
     __syncwarp();
 }
 
@@ -372,7 +378,7 @@ static void launch_band(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles,
         if (per_sm < 1) per_sm = 1;
         grid = blocks_for(tiles, wpb, per_sm * sms);
     }
-    kern<<<grid, 32 * wpb, smem, st>>>(a, tm);
+    launch_k(kern, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
 template <int kCols>
@@ -381,7 +387,7 @@ static void launch_fast_tma(const GenArgs &a, const CUtensorMap &tm, int grid, i
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(v1_fast_kernel<StoreSink, kCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-    v1_fast_kernel<StoreSink, kCols><<<grid, 32 * wpb, smem, st>>>(a, tm);
+    launch_k(v1_fast_kernel<StoreSink, kCols>, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
@@ -405,17 +411,17 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             else launch_fast_tma<16>(a, *tmap, grid, wpb, st);
         } else {
             int grid = blocks_for(tiles, 4, persistent_blocks);
-            v1_fast_kernel<StatsSink, 0><<<grid, 128, 4 * StatsSink::kSmemBytesPerWarp, st>>>(a, *tmap);
+            launch_k(v1_fast_kernel<StatsSink, 0>, dim3(grid), dim3(128), 4 * StatsSink::kSmemBytesPerWarp, st, a, *tmap);
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;
         const int wpb = 8;
         if (mode == 2) {
             int grid = blocks_for(tiles, wpb, persistent_blocks);
-            v1_general_kernel<StatsSink><<<grid, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a);
+            launch_k(v1_general_kernel<StatsSink>, dim3(grid), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
         } else {
             int grid = blocks_for(tiles, wpb, 0);
-            v1_general_kernel<StoreSink><<<grid, 32 * wpb, 0, st>>>(a);
+            launch_k(v1_general_kernel<StoreSink>, dim3(grid), dim3(32 * wpb), 0, st, a);
         }
     }
     return 1;

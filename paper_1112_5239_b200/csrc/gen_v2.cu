@@ -51,6 +51,8 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
 template <class Sink>
 __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t C = a.C;
     const uint32_t off = lane % C, gbase = lane - off;
@@ -114,9 +116,9 @@ int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
-        v2_kernel<StatsSink><<<(int)blocks, 32 * wpb, wpb * StatsSink::kSmemBytesPerWarp, st>>>(a);
+        launch_k(v2_kernel<StatsSink>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
     } else {
-        v2_kernel<StoreSink><<<(int)blocks, 32 * wpb, 0, st>>>(a);
+        launch_k(v2_kernel<StoreSink>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }
     return 1;
 }

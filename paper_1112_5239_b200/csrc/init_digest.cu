@@ -20,6 +20,8 @@ __device__ __forceinline__ uint32_t gcd_u32(uint32_t a, uint32_t b) {
 }
 
 __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint32_t *P = a.state;
     const uint64_t L = a.n_local;
@@ -76,13 +78,15 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
 int launch_init(const InitArgs &a, cudaStream_t st) {
     uint64_t blocks = (a.n_local + 255) / 256;
     if (blocks > 148u * 32u) blocks = 148u * 32u;
-    init_kernel<<<(int)blocks, 256, 0, st>>>(a);
+    launch_k(init_kernel, dim3((int)blocks), dim3(256), 0, st, a);
     return 1;
 }
 
 // ------------------------------------------------------------------ digest
 __global__ void __launch_bounds__(256) digest_kernel(const uint32_t *__restrict__ out, uint64_t first_stream,
                                                      uint64_t total, uint64_t n, uint64_t *digest) {
+    pdl_launch_dependents();
+    pdl_wait();  // previous grid on the stream complete + visible
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t base = first_stream * n;  // global index of out[0]
     uint64_t acc = 0;
@@ -99,7 +103,7 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
     if (total == 0) return 0;
     uint64_t blocks = (total + 255) / 256;
     if (blocks > (uint64_t)grid) blocks = grid;
-    digest_kernel<<<(int)blocks, 256, 0, st>>>(out, first_stream, total, n, digest);
+    launch_k(digest_kernel, dim3((int)blocks), dim3(256), 0, st, out, first_stream, total, n, digest);
     return 1;
 }
 

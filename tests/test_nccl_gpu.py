@@ -30,7 +30,7 @@ def test_torchrun_nccl_consume_matches_oracle(variant):
     S, n, calls = 2048, 64, 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tools", "dist_consume.py"),
-           "--streams", str(S), "--n", str(n), "--calls", str(calls), "--variant", str(variant)]
+           "--streams", str(S), "--rounds", str(n), "--calls", str(calls), "--variant", str(variant)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]

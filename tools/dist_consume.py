@@ -31,7 +31,7 @@ from paper_1112_5239_b200.dist import allreduce_sum_, shard_range  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--streams", type=int, default=W.CONFIGS["C5"]["n_streams"])
-    ap.add_argument("--n", type=int, default=W.CONFIGS["C5"]["n"])
+    ap.add_argument("--rounds", type=int, default=W.CONFIGS["C5"]["n"])
     ap.add_argument("--calls", type=int, default=W.CONFIGS["C5"]["calls"])
     ap.add_argument("--variant", type=int, default=1)
     ap.add_argument("--seed", type=int, default=W.SEEDS[0])
@@ -51,7 +51,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.calls):
-        g.consume(args.n, stats)
+        g.consume(args.rounds, stats)
     allreduce_sum_(stats)
     e1.record()
     torch.cuda.synchronize()
@@ -67,10 +67,10 @@ def main():
         exp = hist.sum() / 256
         chi2 = float(((hist - exp) ** 2 / exp).sum())
         print(json.dumps({
-            "world_size": ws, "variant": args.variant, "streams": args.streams, "n": args.n, "calls": args.calls,
-            "numbers": args.streams * args.n * args.calls,
+            "world_size": ws, "variant": args.variant, "streams": args.streams, "n": args.rounds, "calls": args.calls,
+            "numbers": args.streams * args.rounds * args.calls,
             "seconds_max_over_ranks": float(t.item()),
-            "numbers_per_s": args.streams * args.n * args.calls / float(t.item()),
+            "numbers_per_s": args.streams * args.rounds * args.calls / float(t.item()),
             "pi_hat": 4 * inside / pairs, "pi_z": (inside / pairs - p) / math.sqrt(p * (1 - p) / pairs),
             "hist_chi2_p": float(sst.chi2.sf(chi2, 255)),
             "stats": [int(v) for v in s],
