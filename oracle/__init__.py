@@ -21,9 +21,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ciprng_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-V0, V1, V2 = 0, 1, 2
+V0, V1, V2, V3, V4 = 0, 1, 2, 3, 4
 # words (u32) per stream in the oracle's own structs (see ciprng_oracle.c)
-STATE_WORDS = {V0: 24, V1: 6, V2: 18}
+STATE_WORDS = {V0: 24, V1: 6, V2: 18, V3: 4, V4: 24}
 
 
 def build(force: bool = False) -> str:
@@ -169,7 +169,7 @@ def state_planes(variant: int, states: np.ndarray) -> np.ndarray:
     """The oracle's per-stream structs viewed as the C-ABI's SoA u32 planes
     (include/ciprng.h, "State layout"): plane k holds word k of every stream.
     V0 drops the struct's trailing pad word."""
-    nplanes = {V0: 23, V1: 6, V2: 18}[variant]
+    nplanes = {V0: 23, V1: 6, V2: 18, V3: 4, V4: 24}[variant]
     return np.ascontiguousarray(states[:, :nplanes].T)
 
 

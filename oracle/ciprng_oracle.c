@@ -31,6 +31,9 @@
  *                         I3 (group parity), I4 (split invariance)
  *   orc_v2_*              BBS brute force, hand-traced
  *                         C=1 trace, I6 closure, I7 rotation order 8
+ *   orc_v3_*, orc_v4_*    (NEXT-1) I2 self-cancel => prefix-XOR of the
+ *                         published xor64 / pinned Listing-1 fold, I3 group
+ *                         parity, single-cell injection, hand-traced C=2
  *   orc_stats_words       brute-force recount on tiny inputs; pi estimate
  *   orc_digest_words      parity unpinned (a verification hash defined by
  *                         this build; only its arithmetic is checked)
@@ -300,6 +303,67 @@ void orc_v2_init_one(uint64_t seed, uint64_t s, orc_v2_state *st)
 }
 
 /* ======================================================================== */
+/* V3 and V4: Alg. 4's neighbour combination          */
+/* with other strategy sources.                                  */
+/*  V3: the xor64 of the paper's "optimized versions" ("the    */
+/*      optimized versions use the xor64 described in [Marsaglia2003]").    */
+/*      Reading Q29: Alg. 4's t is 32-bit ("a 32-bits xor-like PRNG */
+/*      has been chosen"), so t = xor64() is C's conversion of the 64-bit   */
+/*      output: its low 32 bits.                                            */
+/*  V4: Listing 1's three generators and six-word fold as the  */
+/*      source: t = lo(t1)^hi(t2)^hi(t3)^lo(t2)^hi(t1)^lo(t3) (reading Q30). */
+/* ======================================================================== */
+typedef struct {
+    uint64_t a;     /* xor64 state                            */
+    uint32_t x;     /* chaotic-iteration state                */
+    uint32_t tp;    /* shared cell: previous round's t (Q8)   */
+} orc_v3_state;
+
+typedef struct {
+    uint64_t a;     /* xorshift (xor64) state                 */
+    uint64_t b[4];  /* xor128 state                           */
+    uint64_t c[5];  /* xorwow shift registers                 */
+    uint64_t d;     /* xorwow Weyl counter                    */
+    uint32_t x;     /* chaotic-iteration state                */
+    uint32_t tp;    /* shared cell                            */
+} orc_v4_state;
+
+/* Seeds (Q11 extended): V3 a = W(s,0) (0 -> Marsaglia's 88172645463325252),
+ * x = lo W(s,1), tp = lo W(s,2).  V4: the generator words exactly as V0
+ * (W(s,0..10) with V0's zero guards), x = lo W(s,11), tp = lo W(s,12). */
+void orc_v3_init_one(uint64_t seed, uint64_t s, orc_v3_state *st)
+{
+    st->a = orc_splitmix_word(seed, s, 0);
+    if (st->a == 0) st->a = 88172645463325252ull;
+    st->x = lo32(orc_splitmix_word(seed, s, 1));
+    st->tp = lo32(orc_splitmix_word(seed, s, 2));
+}
+
+void orc_v4_init_one(uint64_t seed, uint64_t s, orc_v4_state *st)
+{
+    orc_v0_state g;
+    int k;
+    orc_v0_init_one(seed, s, 0, &g);
+    st->a = g.a;
+    for (k = 0; k < 4; k++) st->b[k] = g.b[k];
+    for (k = 0; k < 5; k++) st->c[k] = g.c[k];
+    st->d = g.d;
+    st->x = lo32(orc_splitmix_word(seed, s, 11));
+    st->tp = lo32(orc_splitmix_word(seed, s, 12));
+}
+
+/* The strategy draws ("t = xor-like()"). */
+uint32_t orc_v3_draw(orc_v3_state *st) { return lo32(orc_xor64(&st->a)); }
+
+uint32_t orc_v4_draw(orc_v4_state *st)
+{
+    uint64_t t1 = orc_xor64(&st->a);
+    uint64_t t2 = orc_xor128_64(st->b);
+    uint64_t t3 = orc_xorwow_64(st->c, &st->d);
+    return lo32(t1) ^ hi32(t2) ^ hi32(t3) ^ lo32(t2) ^ hi32(t1) ^ lo32(t3);
+}
+
+/* ======================================================================== */
 /* Grid-level entry points (the oracle's mirror of the C-ABI).              */
 /* variant: 0 = V0, 1 = V1, 2 = V2.  states: array of n_local per-stream    */
 /* structs of the variant's type.  Output is stream-major out[s*n + i] (Q9). */
@@ -309,6 +373,8 @@ size_t orc_state_size(int variant)
     if (variant == 0) return sizeof(orc_v0_state);
     if (variant == 1) return sizeof(orc_v1_state);
     if (variant == 2) return sizeof(orc_v2_state);
+    if (variant == 3) return sizeof(orc_v3_state);
+    if (variant == 4) return sizeof(orc_v4_state);
     return 0;
 }
 
@@ -331,6 +397,16 @@ int orc_grid_init(int variant, uint64_t seed, uint64_t first_stream, uint64_t n_
     if (variant == 2) {
         orc_v2_state *st = (orc_v2_state *)states;
         for (s = 0; s < n_local; s++) orc_v2_init_one(seed, first_stream + s, &st[s]);
+        return ORC_OK;
+    }
+    if (variant == 3) {
+        orc_v3_state *st = (orc_v3_state *)states;
+        for (s = 0; s < n_local; s++) orc_v3_init_one(seed, first_stream + s, &st[s]);
+        return ORC_OK;
+    }
+    if (variant == 4) {
+        orc_v4_state *st = (orc_v4_state *)states;
+        for (s = 0; s < n_local; s++) orc_v4_init_one(seed, first_stream + s, &st[s]);
         return ORC_OK;
     }
     return ORC_EINVAL;
@@ -467,12 +543,55 @@ static int v2_generate(orc_v2_state *st, uint64_t n_local, uint32_t C, const uin
     return ORC_OK;
 }
 
+/* V3 / V4 generate: Alg. 4 exactly as v1_generate above (same default
+ * arrays, Q6; same two-phase lockstep, Q7), only the draw of phase 1 comes
+ * from the variant's source. */
+static int v34_generate(int variant, void *states, uint64_t n_local, uint32_t C, const uint8_t *comb,
+                        uint64_t n, uint32_t *out)
+{
+    uint64_t g0, i;
+    uint32_t l;
+    uint32_t gval[32], tnew[32], o1[32], o2[32];
+    orc_v3_state *s3 = (orc_v3_state *)states;
+    orc_v4_state *s4 = (orc_v4_state *)states;
+    if (C == 0 || C > 32 || n_local % C) return ORC_EINVAL;
+    if (comb == NULL && C != 32) return ORC_EINVAL;
+    for (l = 0; l < C; l++) {
+        if (comb) { o1[l] = comb[l]; o2[l] = comb[C + l]; }
+        else default_comb_v1(l, &o1[l], &o2[l]);
+        if (o1[l] >= C || o2[l] >= C) return ORC_EINVAL;
+    }
+    for (g0 = 0; g0 < n_local; g0 += C) {
+        for (i = 0; i < n; i++) {
+            /* phase 1: every thread draws its strategy source */
+            for (l = 0; l < C; l++)
+                gval[l] = variant == 3 ? orc_v3_draw(&s3[g0 + l]) : orc_v4_draw(&s4[g0 + l]);
+            /* phase 2: combine with the previous round's shared cells */
+            for (l = 0; l < C; l++) {
+                uint32_t tp1 = variant == 3 ? s3[g0 + o1[l]].tp : s4[g0 + o1[l]].tp;
+                uint32_t tp2 = variant == 3 ? s3[g0 + o2[l]].tp : s4[g0 + o2[l]].tp;
+                tnew[l] = gval[l] ^ tp1 ^ tp2;
+            }
+            /* phase 3: commit shared cells, chaotic-iteration update, store */
+            for (l = 0; l < C; l++) {
+                uint32_t *tp = variant == 3 ? &s3[g0 + l].tp : &s4[g0 + l].tp;
+                uint32_t *x = variant == 3 ? &s3[g0 + l].x : &s4[g0 + l].x;
+                *tp = tnew[l];
+                *x = orc_xor_step(*x, tnew[l]);
+                out[(g0 + l) * n + i] = *x;
+            }
+        }
+    }
+    return ORC_OK;
+}
+
 int orc_grid_generate(int variant, void *states, uint64_t n_local, uint32_t C,
                       const uint8_t *comb, uint64_t n, uint32_t *out)
 {
     if (variant == 0) { v0_generate((orc_v0_state *)states, n_local, n, out); return ORC_OK; }
     if (variant == 1) return v1_generate((orc_v1_state *)states, n_local, C, comb, n, out);
     if (variant == 2) return v2_generate((orc_v2_state *)states, n_local, C, comb, n, out);
+    if (variant == 3 || variant == 4) return v34_generate(variant, states, n_local, C, comb, n, out);
     return ORC_EINVAL;
 }
 

@@ -348,7 +348,7 @@ def test_stats_odd_n_rejected():
         O.stats(np.zeros((2, 3), np.uint32))
 
 
-@pytest.mark.parametrize("variant", [O.V0, O.V1, O.V2])
+@pytest.mark.parametrize("variant", [O.V0, O.V1, O.V2, O.V3, O.V4])
 def test_oracle_output_statistics(variant):
     """Frequency / runs / byte chi-square sanity (stand-in for BigCrush,
     P:851-853) and the Monte-Carlo pi estimate within 5 sigma."""
@@ -374,3 +374,113 @@ def test_digest_shard_additive():
     swapped = out.copy()
     swapped[[0, 1]] = swapped[[1, 0]]
     assert O.digest(swapped) != O.digest(out)
+
+
+# ---------------------------------------------------------------- V3 / V4
+# NEXT-1: Alg. 4's combination with the xor64 of the paper's
+# "optimized versions" (V3, reading Q29) and with Listing 1's
+# three-generator fold (V4, reading Q30).
+def _v3_state(rows):
+    """rows of (a, x, tp) -> oracle structs (a.lo, a.hi, x, tp)."""
+    return np.array([[a & M32, a >> 32, x, tp] for a, x, tp in rows], dtype=np.uint32)
+
+
+def test_v3_hand_trace_c2(golden):
+    e = golden["hand_traces"]["v3_c2_trace"]
+    st = _v3_state([(ln["a"], ln["x"], ln["tp"]) for ln in e["lanes"]])
+    comb = np.array(e["comb1"] + e["comb2"], dtype=np.uint8)
+    out = O.generate(O.V3, st, 2, comb_size=2, comb=comb)
+    assert out.tolist() == e["outputs"]
+    assert [int(r[0]) | int(r[1]) << 32 for r in st] == e["a_after"]
+
+
+def test_v3_self_combination_is_prefix_xor_of_xor64(golden):
+    """I2 + I1 with C = 1: x_i = x_{i-1} ^ lo32(xor64_i); the first draw is the
+    published Marsaglia value from its published seed."""
+    e = golden["published_sequences"]["xor64"]
+    x0 = 0x0BADF00D
+    st = _v3_state([(e["seed"], x0, 0x77777777)])
+    out = O.generate(O.V3, st, 6, comb_size=1, comb=np.array([0, 0], np.uint8))[0]
+    assert int(out[0]) == x0 ^ (e["outputs"][0] & M32)
+    prev = x0
+    for i, a in enumerate(O.xor64_seq(e["seed"], 6)):
+        assert int(out[i]) == prev ^ (a & M32)
+        prev = int(out[i])
+
+
+@pytest.mark.parametrize("variant", [O.V3, O.V4])
+@pytest.mark.parametrize("custom", [False, True])
+def test_v34_group_parity(variant, custom):
+    """I3 as for V1: XOR over a group's lanes of t_i equals XOR of the draws
+    g_i, which a C = 1 run (I2: t = g) of the same states exposes."""
+    S, n = 64, 7
+    st = O.init_states(variant, 31, 0, S)
+    xcol = 2 if variant == O.V3 else 22
+    x0 = st[:, xcol].astype(np.uint64)
+    solo = st.copy()
+    g = O.generate(variant, solo, n, comb_size=1, comb=np.zeros(2, np.uint8)).astype(np.uint64)
+    g ^= np.concatenate([x0[:, None], g[:, :-1]], axis=1)
+    comb = W.random_comb(W.rng(4), 32, 2) if custom else None
+    out = O.generate(variant, st, n, comb=comb).astype(np.uint64)
+    t = out ^ np.concatenate([x0[:, None], out[:, :-1]], axis=1)
+    for grp in range(S // 32):
+        sl = slice(32 * grp, 32 * grp + 32)
+        assert np.array_equal(np.bitwise_xor.reduce(t[sl], axis=0), np.bitwise_xor.reduce(g[sl], axis=0))
+
+
+def test_v4_self_combination_is_listing1():
+    """I2 for V4: with C = 1 the shared terms cancel, so V4 is exactly Listing 1
+    (= V0, pinned above to its hand trace and to the fold of the published
+    generators) when both start from the same generator words and x."""
+    v0 = O.init_states(O.V0, 0, 0, 1, paper_defaults=True)
+    v4 = np.zeros((1, 24), np.uint32)
+    v4[0, :23] = v0[0, :23]
+    v4[0, 23] = 0xCAFEBABE  # tp: cancels
+    a = O.generate(O.V0, v0, 40)
+    b = O.generate(O.V4, v4, 40, comb_size=1, comb=np.zeros(2, np.uint8))
+    assert np.array_equal(a, b)
+    assert np.array_equal(v0[0, :23], v4[0, :23])
+
+
+@pytest.mark.parametrize("variant", [O.V3, O.V4])
+def test_v34_default_tables_plus1_plus17(variant):
+    """Q6 defaults shared with V1: a single injected shared cell at lane k
+    reaches exactly lanes k-1 and k-17 in round 0."""
+    S = 32
+    st = O.init_states(variant, 3, 0, S)
+    xcol = 2 if variant == O.V3 else 22
+    st[:, xcol] = 0
+    st[:, xcol + 1] = 0
+    solo = st.copy()
+    g = O.generate(variant, solo, 1, comb_size=1, comb=np.zeros(2, np.uint8))[:, 0].astype(np.uint64)
+    k, T = 9, 0x3C3C3C3C
+    st[k, xcol + 1] = T
+    out = O.generate(variant, st, 1)[:, 0].astype(np.uint64)
+    assert {l for l in range(S) if int(out[l] ^ g[l]) == T} == {(k - 1) % 32, (k - 17) % 32}
+    assert {l for l in range(S) if int(out[l] ^ g[l]) == 0} == set(range(S)) - {(k - 1) % 32, (k - 17) % 32}
+
+
+@pytest.mark.parametrize("variant", [O.V3, O.V4])
+def test_v34_split_and_shard_invariance(variant):
+    st1 = O.init_states(variant, 9, 0, 64)
+    st2 = st1.copy()
+    full = O.generate(variant, st1, 11)
+    part = np.concatenate([O.generate(variant, st2, 4), O.generate(variant, st2, 7)], axis=1)
+    assert np.array_equal(full, part) and np.array_equal(st1, st2)
+    hi = O.generate(variant, O.init_states(variant, 9, 32, 32), 11)
+    assert np.array_equal(full[32:], hi)
+
+
+def test_v34_seeding():
+    """Seeds (Q11 extended): V3 a = W(s,0), x = lo W(s,1), tp = lo W(s,2); V4
+    shares V0's generator words and takes x = lo W(s,11), tp = lo W(s,12)."""
+    st = O.init_states(O.V3, 5, 7, 2)
+    for r, s in enumerate((7, 8)):
+        a = O.splitmix_word(5, s, 0)
+        assert [int(v) for v in st[r]] == [a & M32, a >> 32, O.splitmix_word(5, s, 1) & M32,
+                                          O.splitmix_word(5, s, 2) & M32]
+    v4 = O.init_states(O.V4, 5, 7, 2)
+    v0 = O.init_states(O.V0, 5, 7, 2)
+    assert np.array_equal(v4[:, :22], v0[:, :22])
+    assert v4[:, 22].tolist() == [O.splitmix_word(5, s, 11) & M32 for s in (7, 8)]
+    assert v4[:, 23].tolist() == [O.splitmix_word(5, s, 12) & M32 for s in (7, 8)]

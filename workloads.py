@@ -12,8 +12,9 @@ from __future__ import annotations
 
 import numpy as np
 
-V0, V1, V2 = 0, 1, 2
-VARIANT_NAMES = {V0: "v0_xorlike3", V1: "v1_xor128_comb", V2: "v2_bbs_comb"}
+V0, V1, V2, V3, V4 = 0, 1, 2, 3, 4
+VARIANT_NAMES = {V0: "v0_xorlike3", V1: "v1_xor128_comb", V2: "v2_bbs_comb", V3: "v3_xor64_comb",
+                 V4: "v4_xorlike3_comb"}
 
 # fixed seed list; timing uses the first
 SEEDS = [0x0123456789ABCDEF, 0, 0xFFFFFFFFFFFFFFFF]
