@@ -355,6 +355,13 @@ def measure_secondary(P, torch, dev, args):
     res["v0_store"] = {"value": S0 * n0 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S0, "n": n0}
     g.close()
     del out
+    for name, var in (("v3_store", P.V3), ("v4_store", P.V4)):
+        g = P.ChaoticPRNG(W.SEEDS[0], S0, var)
+        out = torch.empty((S0, n0), dtype=torch.int32, device=dev)
+        s = timed(lambda: g.generate(n0, out=out), 20)
+        res[name] = {"value": S0 * n0 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S0, "n": n0}
+        g.close()
+        del out
     S5, n5 = 2**20, 1024
     g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
     stats = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)

@@ -50,11 +50,19 @@ typedef struct prng_s prng_t; /* opaque; owns the device state */
  *      (Q5); t = xor128() ^ shmem[o1] ^ shmem[o2]; shmem[tid] = t; x ^= t.
  *  V2  Alg. 5 BBS kernel: 8 Blum-Blum-Shub instances, 4 low
  *      bits per squaring, two variable shifts, 16 arrangement arrays chosen
- *      per call, state rotation at exit. */
+ *      per call, state rotation at exit.
+ *  V3 Alg. 4 with the xor64 source of the paper's
+ *      "optimized versions": t = low 32 bits of xor64()
+ *      (reading Q29) ^ shmem[o1] ^ shmem[o2].
+ *  V4  (NEXT-1) Alg. 4 with Listing 1's three generators and six-word fold
+ *       as the strategy source (reading Q30).
+ * V3 and V4 take Alg. 4's two combination arrays exactly like V1. */
 enum prng_variant {
     PRNG_V0_XORLIKE3 = 0,
     PRNG_V1_XOR128_COMB = 1,
-    PRNG_V2_BBS_COMB = 2
+    PRNG_V2_BBS_COMB = 2,
+    PRNG_V3_XOR64_COMB = 3,
+    PRNG_V4_XORLIKE3_COMB = 4
 };
 
 enum prng_status {
@@ -78,7 +86,8 @@ enum prng_store_path {
 
 typedef struct prng_config {
     /* combination_size C (reading Q6): 0 = default 32.
-     * Must be 1, 2, 4, 8, 16 or 32 (a group never straddles a warp). */
+     * Must be 1, 2, 4, 8, 16 or 32 (a group never straddles a warp).
+     * V3 and V4 use V1's two arrays and defaults. */
     uint32_t comb_size;
     /* HOST pointer, copied at creation.  V1: 2*C entries, array_comb1 then
      * array_comb2.  V2: 16*C entries, array_comb[0..15][0..C-1]
@@ -110,7 +119,7 @@ CIPRNG_API int prng_create(uint64_t seed, uint64_t n_streams, int variant, prng_
  * how streams are sharded over handles or GPUs.
  * Errors: PRNG_EINVAL if variant unknown, n_local == 0, out == NULL,
  * comb_size not a power of two <= 32, a table entry >= C, comb == NULL with
- * C != 32, V1/V2 with first_stream % C or n_local % C != 0 (groups must be
+ * C != 32, V1-V4 with first_stream % C or n_local % C != 0 (groups must be
  * complete), paper_defaults with anything but V0 and
  * (first_stream, n_local) == (0, 1) (Q26). PRNG_ENOMEM, PRNG_ECUDA. */
 CIPRNG_API int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, int variant,
@@ -158,7 +167,8 @@ CIPRNG_API int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *ou
  *   [2 + b] count of x with x >> 24 == b, b = 0..255.
  * Integer sums, so results are independent of launch shape and of how
  * streams are sharded (the multi-GPU all-reduce is bit-exact).
- * Errors: PRNG_EINVAL if n is odd or a pointer is NULL, PRNG_ECUDA. */
+ * Errors: PRNG_EINVAL if n is odd or a pointer is NULL, PRNG_ESIZE if
+ * n >= 2^31 (split the call; V0/V1 are split invariant), PRNG_ECUDA. */
 CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
 
 /* Verification digest of one call's output block (reading Q28):
@@ -176,7 +186,7 @@ typedef struct prng_info_t {
     int32_t variant;
     uint32_t comb_size;
     uint64_t seed, first_stream, n_local;
-    uint32_t state_words; /* u32 planes per stream (V0 23, V1 6, V2 18) */
+    uint32_t state_words; /* u32 planes per stream (V0 23, V1 6, V2 18, V3 4, V4 24) */
     int32_t device;
     int32_t store_path;   /* path used by the last prng_generate */
     uint32_t kernel_launches; /* kernels launched by the last call */
@@ -192,6 +202,8 @@ CIPRNG_API int prng_get_info(const prng_t *h, prng_info_t *info);
  *  V2 (18): y1..y8 (BBS states) | m1..m8 (index of each instance's modulus
  *           in the ascending table of the 78 products p*q, p < q primes = 3
  *           mod 4 in [128, 256], Q13) | x | tp
+ *  V3 (4):  a.lo a.hi (xor64) | x | tp
+ *  V4 (24): V0's 22 generator words | x | tp
  * get/set copy exactly state_words*n_local*4 bytes (else PRNG_ESTATE) and
  * synchronise the device.  set_state is the checkpoint-resume hook (P:905:
  * the state written back after every kernel is a checkpoint). */

@@ -27,11 +27,11 @@ from ._lib import (  # noqa: F401
     lib,
 )
 
-V0, V1, V2 = 0, 1, 2
-STATE_WORDS = {V0: 23, V1: 6, V2: 18}
+V0, V1, V2, V3, V4 = 0, 1, 2, 3, 4
+STATE_WORDS = {V0: 23, V1: 6, V2: 18, V3: 4, V4: 24}
 N_STATS = 258
 
-__all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "STATE_WORDS", "N_STATS", "lib", "PrngError"]
+__all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "V3", "V4", "STATE_WORDS", "N_STATS", "lib", "PrngError"]
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
@@ -44,7 +44,9 @@ class ChaoticPRNG:
     """Per-stream chaotic-iteration generators for global streams
     [first, first + n_local) of the stream space of ``seed``.
 
-    variant: V0 (Listing 1 / Alg. 3), V1 (Alg. 4), V2 (Alg. 5, BBS).
+    variant: V0 (Listing 1 / Alg. 3), V1 (Alg. 4), V2 (Alg. 5, BBS), V3 (Alg. 4 with
+    the xor64 source of the paper's optimized kernels), V4 (Alg. 4 with Listing
+    1's three-generator fold as the source).
     comb_size / comb: combination arrays (None = default C = 32 tables).
     """
 

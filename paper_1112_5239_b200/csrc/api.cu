@@ -44,7 +44,9 @@ struct DeviceGuard {
 
 // Modulus table of V2 (reading Q13), built here independently of any other
 // component: primes p = 3 (mod 4) in [128, 256] by a sieve, products p < q
-// ascending, each with its Barrett constant mu = floor(2^32 / M).
+// ascending, each as one 16-byte entry {M, mu = floor(2^32 / M), 2^32 - M, 0}
+// (one 128-bit load per BBS instance; the negated modulus is stored rather
+// than derived so the kernel's Barrett step stays 3 IMAD + 1 VIADDMNMX).
 std::vector<uint32_t> modulus_table() {
     std::vector<bool> composite(257, false);
     std::vector<uint32_t> primes;
@@ -61,6 +63,8 @@ std::vector<uint32_t> modulus_table() {
     for (uint32_t M : Ms) {
         tab.push_back(M);
         tab.push_back((uint32_t)((1ull << 32) / M));
+        tab.push_back(0u - M);
+        tab.push_back(0u);
     }
     return tab;
 }
@@ -83,7 +87,7 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-constexpr int kStateWords[3] = {23, 6, 18};
+constexpr int kStateWords[5] = {23, 6, 18, 4, 24};
 
 }  // namespace
 
@@ -211,8 +215,26 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
             }
         }
         launches = launch_v1(a, fast, kmode, tm, st, h->persistent_blocks, tune);
-    } else {
+    } else if (h->variant == 2) {
         launches = launch_v2(a, mode, st, h->persistent_blocks);
+    } else if (h->variant == 3) {
+        const bool fast = h->default_tables && h->C == 32;
+        int kmode = mode;
+        const CUtensorMap *tm = nullptr;
+        if (mode == 0 && fast) {
+            const bool tma_ok = a.vec && n < (1ull << 31) && s_count < (1ull << 31);
+            if (h->store_path == PRNG_STORE_TMA && reinterpret_cast<uintptr_t>(out) % 16 != 0) return PRNG_EALIGN;
+            if (h->store_path != PRNG_STORE_DIRECT && tma_ok) {
+                tm = tensor_map(h, out, n, s_count, 32);
+                if (tm) {
+                    kmode = 1;
+                    path = PRNG_STORE_TMA;
+                }
+            }
+        }
+        launches = launch_v3(a, fast, kmode, tm, st, h->persistent_blocks);
+    } else {
+        launches = launch_v4(a, mode, st, h->persistent_blocks);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
@@ -235,7 +257,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
                       prng_t **out) {
     if (out == nullptr) return PRNG_EINVAL;
     *out = nullptr;
-    if (variant < 0 || variant > 2 || n_local == 0) return PRNG_EINVAL;
+    if (variant < 0 || variant > 4 || n_local == 0) return PRNG_EINVAL;
     uint32_t C = 32;
     const uint8_t *comb = nullptr;
     int paper_defaults = 0, store_path = PRNG_STORE_AUTO;
@@ -260,7 +282,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
             delete h;
             return PRNG_EINVAL;
         }
-        const int ntab = variant == 1 ? 2 : 16;
+        const int ntab = variant == 2 ? 16 : 2;
         for (int t = 0; t < ntab; ++t)
             for (uint32_t l = 0; l < C; ++l) {
                 uint32_t v;
@@ -270,7 +292,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
                         delete h;
                         return PRNG_EINVAL;
                     }
-                } else if (variant == 1) {
+                } else if (variant != 2) {  // V1, V3, V4: Alg. 4's two arrays
                     v = (t == 0) ? (l + 1u) % 32u : (l + 17u) % 32u;  // Q6
                 } else {
                     v = (t < 8) ? (l + 1u + t) % 32u : (l + 17u + (t - 8)) % 32u;  // Q6
@@ -310,7 +332,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         return PRNG_ENOMEM;
     }
     std::vector<uint32_t> tab = modulus_table();
-    h->n_mod = (uint32_t)(tab.size() / 2);
+    h->n_mod = (uint32_t)(tab.size() / 4);
     e = cudaMalloc(&h->mod, tab.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(h->mod, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -435,6 +457,7 @@ int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *st
     if (!h || !stats_dev || (n_per_stream & 1)) return PRNG_EINVAL;
     h->last_launches = 0;
     if (n_per_stream == 0) return PRNG_OK;
+    if (n_per_stream >= (1ull << 31)) return PRNG_ESIZE;  // per-lane u32 pair counters
     DeviceGuard g(h->device);
     return run_pass(h, n_per_stream, 0, h->n_local, nullptr, stats_dev, 2, (cudaStream_t)stream);
 }
@@ -503,10 +526,11 @@ int prng_selftest_modsq(uint64_t *mismatches) {
     if (!mismatches) return PRNG_EINVAL;
     std::vector<uint32_t> tab = modulus_table();
     uint64_t bad = 0;
-    for (size_t k = 0; k + 1 < tab.size(); k += 2) {
-        const uint32_t M = tab[k], mu = tab[k + 1];
+    for (size_t k = 0; k + 3 < tab.size(); k += 4) {
+        const uint32_t M = tab[k], mu = tab[k + 1], nM = tab[k + 2];
+        if (nM != 0u - M) ++bad;
         for (uint32_t y = 0; y < M; ++y)
-            if (barrett_sq(y, 0u - M, mu) != (y * y) % M) ++bad;
+            if (barrett_sq(y, nM, mu) != (y * y) % M) ++bad;
     }
     *mismatches = bad;
     return PRNG_OK;

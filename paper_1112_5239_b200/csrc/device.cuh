@@ -30,9 +30,23 @@ __host__ __device__ __forceinline__ uint64_t seed_word(uint64_t seed, uint64_t s
 // Marsaglia xor128 on 32-bit words (Alg. 4 source), written as
 // the 4-term recurrence w_{k+4} = f(w_k, w_{k+3}) so an unroll-by-4 loop
 // keeps the state in a register ring with no moves.
+// Constant right shift as a high multiply (IMAD.HI on the heavy FMA
+// sub-pipe) instead of SHF on the ALU pipe.  Inline PTX so the compiler
+// cannot canonicalise it back into SHF.  Pipe costs measured with ncu (r1d):
+// an ALU op or IMAD/IMAD.SHL holds its pipe 2 cycles per warp, IMAD.HI 4.
+template <int k>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t v) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "n"(1u << (32 - k)));
+    return r;
+}
+// xor128 step with the pipes balanced: x << 11 is IMAD.SHL, w >> 19 is
+// IMAD.HI, t >> 8 stays SHF; with the combination's LOP3s the V1 kernels
+// spend ~11 ALU and ~6 heavy-FMA cycles per warp-number (all shifts on SHF:
+// 13 / 2; both right shifts as IMAD.HI: 9 / 10).
 __device__ __forceinline__ uint32_t xor128_f(uint32_t xk, uint32_t wk3) {
     uint32_t t = xk ^ (xk << 11);
-    return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
+    return (wk3 ^ shr_fma<19>(wk3)) ^ (t ^ (t >> 8));
 }
 // Same on 64-bit words (Listing 1's xor128, reading Q2).
 __device__ __forceinline__ uint64_t xor128_f64(uint64_t xk, uint64_t wk3) {
@@ -108,6 +122,18 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Byte offset of 16-byte chunk c of row r in a tile of kCols u32 columns
+// (row pitch P = 4 kCols bytes) written with CU_TENSOR_MAP_SWIZZLE_{P}B:
+// the chunk index is XORed with address bits [7, 7 + log2(P/16)), i.e. with
+// (r * P / 128) mod (P / 16).  For every P this makes the 8 lanes of one
+// STS.128 phase (8 consecutive rows, same chunk) hit 8 distinct 16-byte
+// bank groups.
+template <int kCols>
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
+    constexpr uint32_t P = kCols * 4;
+    return r * P + ((c ^ ((r * P >> 7) & (P / 16 - 1))) << 4);
+}
+
 // ------------------------------------------- programmatic dependent launch
 // Every kernel is launched with programmatic stream serialization (PDL): it
 // lets the next kernel on the stream be scheduled while this one drains, and
@@ -136,7 +162,7 @@ struct GenArgs {
     uint64_t n;          // rounds per stream
     uint32_t *out;       // row 0 = stream s_begin; row stride n (store kernels)
     uint64_t *stats;     // consume kernels: 258 u64
-    const uint32_t *mod; // V2: [78][2] = {M, mu}
+    const uint32_t *mod; // V2: [78][4] = {M, mu, 2^32 - M, 0}
     uint32_t C;          // combination_size
     uint32_t vec;        // 1: rows are 16-byte aligned, n % 4 == 0
     CombTables comb;
@@ -150,6 +176,10 @@ namespace ciprng {
 // 64-bit constant shift is one funnel shift (ALU pipe) plus one plain 32-bit
 // shift expressed as a multiply (IMAD.SHL / IMAD.HI: FMA pipe).  Same values
 // as the uint64_t forms above; this only balances the two integer pipes.
+// Measured (ncu r1d): IMAD.HI occupies the heavy FMA sub-pipe twice as long
+// as IMAD.SHL or an ALU op, so writing the funnel halves as multiplies too
+// (IMAD.SHL + IMAD.HI, merged by XOR) made V0 heavy-pipe bound and 15 %
+// slower; this split is the measured optimum.
 struct u64p {
     uint32_t lo, hi;
 };

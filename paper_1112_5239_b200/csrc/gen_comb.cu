@@ -1,0 +1,266 @@
+// gen_comb.cu -- V3: Alg. 4's neighbour combination
+// with the xor64 source of the paper's "optimized versions" (P:1026-1028,
+// "the optimized versions use the xor64 described in [Marsaglia2003]"),
+// SURVEY s8(f) NEXT-1 (i).  Reading Q29: Alg. 4's t is a 32-bit word
+// (P:950), so t = xor64() takes the low 32 bits of the 64-bit output.
+//
+// Per stream: xor64 state a (two u32 halves), x, the shared cell tp.  Per
+// round:  t = lo(xor64(a)) ^ tp[o1] ^ tp[o2];  tp = t;  x ^= t;  emit x.
+//
+// The kernels are templated on the strategy source (`Src`): the exchange,
+// store and consume machinery is the V1 design (gen_v1.cu) --
+//  * comb_general_kernel: any C | 32 and any arrays, one lane per stream,
+//    two SHFL.IDX per number;
+//  * comb_fast_kernel: the default arrays comb1 = l+1, comb2 = l+17 (Q6):
+//    lane j of a half-warp owns streams j and j+16, one width-16 SHFL per
+//    two numbers (u[j] = tp[j] ^ tp[j+16] trick, see gen_v1.cu), and either
+//    128-bit STG or 64-stream x 32-round TMA tiles (2-D bulk tensor store).
+#include "device.cuh"
+#include "kernels.h"
+#include "sinks.cuh"
+
+namespace ciprng {
+
+// Marsaglia xor64 (13, 7, 17) on (lo, hi) halves (device.cuh u64p helpers:
+// funnel halves on SHF, plain halves as IMAD.SHL / IMAD.HI).
+struct SrcXor64 {
+    static constexpr int kPlanes = 2;  // a.lo, a.hi; then x, tp
+    u64p a;
+    __device__ __forceinline__ void load(const uint32_t *P, uint64_t L, uint64_t s) {
+        a.lo = P[0 * L + s];
+        a.hi = P[1 * L + s];
+    }
+    __device__ __forceinline__ void store(uint32_t *P, uint64_t L, uint64_t s) const {
+        P[0 * L + s] = a.lo;
+        P[1 * L + s] = a.hi;
+    }
+    __device__ __forceinline__ void zero() { a = {0u, 0u}; }
+    __device__ __forceinline__ uint32_t next() {
+        a = xor64_step_p(a);
+        return a.lo;  // Q29
+    }
+};
+
+// ===================================================================== general
+template <class Src, class Sink>
+__global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
+    constexpr int X = Src::kPlanes, TP = Src::kPlanes + 1;
+    Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t C = a.C;
+    const uint32_t off = lane % C, gbase = lane - off;
+    const uint32_t src1 = gbase + a.comb.t[0][off];
+    const uint32_t src2 = gbase + a.comb.t[1][off];
+    const uint64_t n_tiles = (a.s_count + 31) / 32;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *P = a.state;
+    const uint64_t L = a.n_local;
+
+    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
+         tile += warps) {
+        const uint64_t row = tile * 32 + lane;
+        const bool valid = row < a.s_count;
+        const uint64_t s = a.s_begin + row;
+        Src g;
+        uint32_t x = 0, tp = 0;
+        g.zero();
+        if (valid) {
+            g.load(P, L, s);
+            x = P[X * L + s];
+            tp = P[TP * L + s];
+        }
+        sink.begin_row(0, row);
+        auto round = [&]() -> uint32_t {
+            const uint32_t t = g.next() ^ __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
+            tp = t;
+            x ^= t;
+            return x;
+        };
+        uint64_t i = 0;
+        for (; i + 4 <= a.n; i += 4) {
+            const uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
+            sink.put4(0, i, o0, o1, o2, o3, valid);
+        }
+        for (; i < a.n; ++i) sink.put1(0, i, round(), valid);
+        sink.end_rows(valid ? 1u : 0u);
+        if (valid) {
+            g.store(P, L, s);
+            P[X * L + s] = x;
+            P[TP * L + s] = tp;
+        }
+    }
+    sink.finish(a);
+}
+
+// ======================================================================== fast
+constexpr int kCombTileRows = 64;
+
+template <class Src, class Sink, int kCols>
+__global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+    constexpr int X = Src::kPlanes, TP = Src::kPlanes + 1;
+    constexpr bool kTma = kCols > 0;
+    constexpr uint32_t kTileBytes = kCombTileRows * (kCols > 0 ? kCols : 4) * 4;
+    Sink sink(a);
+    pdl_launch_dependents();
+    pdl_wait();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t h = lane >> 4, j = lane & 15u;
+    const uint32_t src = (j + 1u) & 15u;
+    const uint64_t n_tiles = (a.s_count + kCombTileRows - 1) / kCombTileRows;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *P = a.state;
+    const uint64_t L = a.n_local;
+    const uint32_t rA_t = 32u * h + j, rB_t = rA_t + 16u;
+
+    uint32_t wsmem = 0;
+    if constexpr (kTma) {
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        const uint32_t base = (smem_u32(smem_dyn) + 1023u) & ~1023u;
+        wsmem = base + (threadIdx.x >> 5) * (2 * kTileBytes);
+    }
+    uint32_t issued = 0;
+
+    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
+         tile += warps) {
+        const uint64_t row0 = tile * kCombTileRows;
+        const bool valid = row0 + 32u * h < a.s_count;
+        const uint64_t rA = row0 + rA_t, rB = row0 + rB_t;
+        const uint64_t sA = a.s_begin + rA, sB = a.s_begin + rB;
+        Src gA, gB;
+        uint32_t xA = 0, tpA = 0, xB = 0, tpB = 0;
+        gA.zero();
+        gB.zero();
+        if (valid) {
+            gA.load(P, L, sA);
+            gB.load(P, L, sB);
+            xA = P[X * L + sA]; tpA = P[TP * L + sA];
+            xB = P[X * L + sB]; tpB = P[TP * L + sB];
+        }
+        sink.begin_row(0, rA);
+        sink.begin_row(1, rB);
+        uint32_t u = tpA ^ tpB, nb = 0, lastA = 0, lastB = 0;
+        // one round for both of the lane's streams: u[j] = t[j] ^ t[j+16] of
+        // the previous round; both streams need tp[j+1] ^ tp[j+17] = u[j+1]
+        auto round2 = [&](uint32_t &oA, uint32_t &oB) {
+            lastA = gA.next();
+            lastB = gB.next();
+            nb = __shfl_sync(kFull, u, src, 16);
+            xA ^= lastA ^ nb;
+            xB ^= lastB ^ nb;
+            u = lastA ^ lastB;
+            oA = xA;
+            oB = xB;
+        };
+        uint64_t i = 0;
+        if constexpr (kTma) {
+            for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
+                const uint32_t buf = wsmem + (issued & 1u) * kTileBytes;
+                if (issued >= 2) {
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                }
+                const uint32_t q_end = (i0 + kCols <= a.n) ? kCols / 4 : (uint32_t)((a.n - i0) / 4);
+#pragma unroll 8
+                for (uint32_t q = 0; q < q_end; ++q) {
+                    uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
+                    round2(oA0, oB0);
+                    round2(oA1, oB1);
+                    round2(oA2, oB2);
+                    round2(oA3, oB3);
+                    st_shared_v4(buf + swz<kCols>(rA_t, q), oA0, oA1, oA2, oA3);
+                    st_shared_v4(buf + swz<kCols>(rB_t, q), oB0, oB1, oB2, oB3);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmap, buf, (int)i0, (int)row0);
+                    bulk_commit();
+                }
+                ++issued;
+            }
+            i = a.n;
+        } else {
+            for (; i + 4 <= a.n; i += 4) {
+                uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
+                round2(oA0, oB0);
+                round2(oA1, oB1);
+                round2(oA2, oB2);
+                round2(oA3, oB3);
+                sink.put4(0, i, oA0, oA1, oA2, oA3, valid);
+                sink.put4(1, i, oB0, oB1, oB2, oB3, valid);
+            }
+            for (; i < a.n; ++i) {
+                uint32_t oA, oB;
+                round2(oA, oB);
+                sink.put1(0, i, oA, valid);
+                sink.put1(1, i, oB, valid);
+            }
+        }
+        sink.end_rows(valid ? 2u : 0u);
+        if (valid) {
+            if (a.n > 0) {  // last round's t = g ^ nb
+                tpA = lastA ^ nb;
+                tpB = lastB ^ nb;
+            }
+            gA.store(P, L, sA);
+            gB.store(P, L, sB);
+            P[X * L + sA] = xA; P[TP * L + sA] = tpA;
+            P[X * L + sB] = xB; P[TP * L + sB] = tpB;
+        }
+    }
+    if constexpr (kTma) {
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+    }
+    sink.finish(a);
+}
+
+// ===================================================================== launch
+static int comb_blocks(uint64_t warps_needed, int wpb, int cap) {
+    uint64_t b = (warps_needed + wpb - 1) / wpb;
+    if (cap > 0 && b > (uint64_t)cap) b = cap;
+    return (int)(b ? b : 1);
+}
+
+template <class Src>
+static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
+                       int persistent_blocks) {
+    // mode: 0 store-direct, 1 store-tma, 2 consume
+    if (a.s_count == 0) return 0;
+    CUtensorMap dummy;
+    if (tmap == nullptr) tmap = &dummy;
+    if (fast) {
+        const uint64_t tiles = (a.s_count + kCombTileRows - 1) / kCombTileRows;
+        if (mode == 1) {
+            constexpr int kCols = 32, wpb = 2;
+            const size_t smem = (size_t)wpb * 2 * kCombTileRows * kCols * 4 + 1024;
+            auto kern = comb_fast_kernel<Src, StoreSink, kCols>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_k(kern, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), smem, st, a, *tmap);
+        } else if (mode == 0) {
+            launch_k(comb_fast_kernel<Src, StoreSink, 0>, dim3(comb_blocks(tiles, 4, 0)), dim3(128), 0, st, a, *tmap);
+        } else {
+            launch_k(comb_fast_kernel<Src, StatsSink, 0>, dim3(comb_blocks(tiles, 4, persistent_blocks)), dim3(128),
+                     4 * StatsSink::kSmemBytesPerWarp, st, a, *tmap);
+        }
+    } else {
+        const uint64_t tiles = (a.s_count + 31) / 32;
+        const int wpb = 8;
+        if (mode == 2) {
+            launch_k(comb_general_kernel<Src, StatsSink>, dim3(comb_blocks(tiles, wpb, persistent_blocks)),
+                     dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+        } else {
+            launch_k(comb_general_kernel<Src, StoreSink>, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), 0, st, a);
+        }
+    }
+    return 1;
+}
+
+int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
+              int persistent_blocks) {
+    return launch_comb<SrcXor64>(a, fast, mode, tmap, st, persistent_blocks);
+}
+
+}  // namespace ciprng

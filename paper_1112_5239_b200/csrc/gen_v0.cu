@@ -9,6 +9,11 @@
 // become SHF/LOP3 pairs; the xor128 (period-4 register ring) and xorwow
 // (period-5 ring) recurrences are unrolled 20 rounds deep so the state never
 // moves between registers.  Integer-issue bound, not HBM bound.
+//
+// kComb = true is V4 (reading Q30): the same fold
+// f is Alg. 4's strategy source, t = f ^ tp[o1] ^ tp[o2]; tp = t; x ^= t
+// (P:971-974), the group's shared cells exchanged by two SHFL.IDX per number
+// (any C | 32 and any arrays; the draw, not the shuffle, is the cost here).
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -20,12 +25,14 @@ __device__ __forceinline__ uint32_t fold6(uint64_t t1, uint64_t t2, uint64_t t3)
            (uint32_t)t3;
 }
 
-template <class Sink>
+template <class Sink, bool kComb>
 __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t off = lane % a.C, gbase = lane - off;  // V4 only
+    const uint32_t src1 = gbase + a.comb.t[0][off], src2 = gbase + a.comb.t[1][off];
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     uint32_t *P = a.state;
@@ -37,7 +44,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
         const bool valid = row < a.s_count;
         const uint64_t s = a.s_begin + row;
         uint64_t ra = 0, rb[4] = {0, 0, 0, 0}, rc[5] = {0, 0, 0, 0, 0}, rd = 0;
-        uint32_t x = 0;
+        uint32_t x = 0, tp = 0;
         auto ld64 = [&](int k) -> uint64_t {
             return (uint64_t)P[(2 * k) * L + s] | ((uint64_t)P[(2 * k + 1) * L + s] << 32);
         };
@@ -49,7 +56,18 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             for (int k = 0; k < 5; ++k) rc[k] = ld64(5 + k);
             rd = ld64(10);
             x = P[22 * L + s];
+            if (kComb) tp = P[23 * L + s];
         }
+        // x ^= f (V0), or Alg. 4's combination with f as the source (V4)
+        auto update = [&](uint32_t f) {
+            if constexpr (kComb) {
+                const uint32_t t = f ^ __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
+                tp = t;
+                x ^= t;
+            } else {
+                x ^= f;
+            }
+        };
         sink.begin_row(0, row);
         uint64_t i = 0;
         for (; i + 20 <= a.n; i += 20) {
@@ -70,7 +88,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
                 pc[k % 5] = xorwow_f64p(pc[k % 5], pc[(k + 4) % 5]);
                 pd = add64p(pd, weyl);
                 const u64p t3 = add64p(pd, pc[k % 5]);
-                x ^= pa.lo ^ pb[k % 4].hi ^ t3.hi ^ pb[k % 4].lo ^ pa.hi ^ t3.lo;
+                update(pa.lo ^ pb[k % 4].hi ^ t3.hi ^ pb[k % 4].lo ^ pa.hi ^ t3.lo);
                 o[k % 4] = x;
                 if (k % 4 == 3) sink.put4(0, i + k - 3, o[0], o[1], o[2], o[3], valid);
             }
@@ -89,7 +107,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             uint64_t nc = xorwow_f64(rc[0], rc[4]);
             rc[0] = rc[1]; rc[1] = rc[2]; rc[2] = rc[3]; rc[3] = rc[4]; rc[4] = nc;
             rd += 362437u;
-            x ^= fold6(ra, nb, rd + nc);
+            update(fold6(ra, nb, rd + nc));
             return x;
         };
         for (; i + 4 <= a.n; i += 4) {
@@ -97,6 +115,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             sink.put4(0, i, o0, o1, o2, o3, valid);
         }
         for (; i < a.n; ++i) sink.put1(0, i, step(), valid);
+        sink.end_rows(valid ? 1u : 0u);
         if (valid) {
             auto st64 = [&](int k, uint64_t v) {
                 P[(2 * k) * L + s] = (uint32_t)v;
@@ -109,23 +128,34 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             for (int k = 0; k < 5; ++k) st64(5 + k, rc[k]);
             st64(10, rd);
             P[22 * L + s] = x;
+            if (kComb) P[23 * L + s] = tp;
         }
     }
     sink.finish(a);
 }
 
-int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+template <bool kComb>
+static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
     const int wpb = 8;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
-        launch_k(v0_kernel<StatsSink>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+        launch_k(v0_kernel<StatsSink, kComb>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp,
+                 st, a);
     } else {
-        launch_k(v0_kernel<StoreSink>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
+        launch_k(v0_kernel<StoreSink, kComb>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }
     return 1;
+}
+
+int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+    return launch_v0x<false>(a, mode, st, persistent_blocks);
+}
+
+int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+    return launch_v0x<true>(a, mode, st, persistent_blocks);
 }
 
 }  // namespace ciprng

@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
             tp = t; x ^= t;
             sink.put1(0, i, x, valid);
         }
+        sink.end_rows(valid ? 1u : 0u);
         if (valid) {
             P[0 * L + s] = g0; P[1 * L + s] = g1; P[2 * L + s] = g2; P[3 * L + s] = g3;
             P[4 * L + s] = x; P[5 * L + s] = tp;
@@ -89,17 +90,6 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
 // j = L & 15, owns rows rA = 32h + j and rB = rA + 16 of the tile.
 constexpr int kFastTileRows = 64;
 
-// Byte offset of 16-byte chunk c of row r in a tile of kCols u32 columns
-// (row pitch P = 4 kCols bytes) written with CU_TENSOR_MAP_SWIZZLE_{P}B:
-// the chunk index is XORed with address bits [7, 7 + log2(P/16)), i.e. with
-// (r * P / 128) mod (P / 16).  For every P this makes the 8 lanes of one
-// STS.128 phase (8 consecutive rows, same chunk) hit 8 distinct 16-byte
-// bank groups.
-template <int kCols>
-__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
-    constexpr uint32_t P = kCols * 4;
-    return r * P + ((c ^ ((r * P >> 7) & (P / 16 - 1))) << 4);
-}
 
 // kCols == 0: direct stores through the Sink (StoreSink: 128-bit STG per
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
@@ -129,20 +119,30 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
     }
     uint32_t tma_issued = 0;  // boxes issued by this warp
 
-    for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
-         tile += warps) {
+    // State of the warp's NEXT tile is loaded into registers while the current
+    // one computes (ncu r1e: the first use of freshly loaded state was 18 % of
+    // all warp stall samples when every tile waited for its own loads).
+    uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t pa[6] = {0, 0, 0, 0, 0, 0}, pb[6] = {0, 0, 0, 0, 0, 0};
+    auto prefetch = [&](uint64_t t) {
+        if (t < n_tiles && t * kFastTileRows + 32u * h < a.s_count) {
+            const uint64_t sA = a.s_begin + t * kFastTileRows + rA_t, sB = sA + 16u;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                pa[k] = P[k * L + sA];
+                pb[k] = P[k * L + sB];
+            }
+        }
+    };
+    prefetch(tile);
+    for (; tile < n_tiles; tile += warps) {
         const uint64_t row0 = tile * kFastTileRows;
         const bool valid = row0 + 32u * h < a.s_count;  // s_count % 32 == 0
         const uint64_t rA = row0 + rA_t, rB = row0 + rB_t;
         const uint64_t sA = a.s_begin + rA, sB = a.s_begin + rB;
-        uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, xA = 0, tpA = 0;
-        uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0, xB = 0, tpB = 0;
-        if (valid) {
-            a0 = P[0 * L + sA]; a1 = P[1 * L + sA]; a2 = P[2 * L + sA]; a3 = P[3 * L + sA];
-            xA = P[4 * L + sA]; tpA = P[5 * L + sA];
-            b0 = P[0 * L + sB]; b1 = P[1 * L + sB]; b2 = P[2 * L + sB]; b3 = P[3 * L + sB];
-            xB = P[4 * L + sB]; tpB = P[5 * L + sB];
-        }
+        uint32_t a0 = pa[0], a1 = pa[1], a2 = pa[2], a3 = pa[3], xA = pa[4], tpA = pa[5];
+        uint32_t b0 = pb[0], b1 = pb[1], b2 = pb[2], b3 = pb[3], xB = pb[4], tpB = pb[5];
+        prefetch(tile + warps);
         sink.begin_row(0, rA);
         sink.begin_row(1, rB);
         uint32_t u = tpA ^ tpB;  // u[j] = tp[j] ^ tp[j+16]
@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
         }
 #undef CIPRNG_V1_BLOCK4
 #undef CIPRNG_V1_ROUND
+        sink.end_rows(valid ? 2u : 0u);
         if (valid) {
             if (a.n > 0) {
                 // last round's t = g ^ nb; g is the newest ring entry, a3 / b3

@@ -27,24 +27,40 @@ struct Bbs8 {
     uint32_t y[8], nM[8], mu[8];  // nM = 2^32 - M
 };
 
+// bmsk: the low `n` bits set (n in 0..3 here), one BMSK instruction
+__device__ __forceinline__ uint32_t low_mask(uint32_t n) {
+    uint32_t m;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(n));
+    return m;
+}
+
+// One number's strategy word.  The eight 4-bit fields are
+// placed independently (y_j << (28 - 4j), the multiply on the FMA pipe) and
+// merged by a 3-level LOP3 tree -- (hi & mask) | (lo & ~mask) -- instead of
+// the serial t = (t << 4) | nibble chain: same word, depth 3 instead of 8.
+// Each term y_j << (28 - 4j) is zero below its field, so ~mask keeps only
+// the lower operand's fields.
 __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
-    uint32_t t = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
-        t = (t << 4) | (b.y[j] & 15u);
-    }
-    uint32_t sh;
+    for (int j = 0; j < 8; ++j) b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
+    const uint32_t f0 = b.y[0] << 28, f1 = b.y[1] << 24, f2 = b.y[2] << 20, f3 = b.y[3] << 16;
+    const uint32_t f4 = b.y[4] << 12, f5 = b.y[5] << 8, f6 = b.y[6] << 4, f7 = b.y[7];
+    const uint32_t p01 = (f0 & 0xF0000000u) | (f1 & ~0xF0000000u);
+    const uint32_t p23 = (f2 & 0xFFF00000u) | (f3 & ~0xFFF00000u);
+    const uint32_t p45 = (f4 & 0xFFFFF000u) | (f5 & ~0xFFFFF000u);
+    const uint32_t p67 = (f6 & 0xFFFFFFF0u) | (f7 & ~0xFFFFFFF0u);
+    const uint32_t p03 = (p01 & 0xFF000000u) | (p23 & ~0xFF000000u);
+    const uint32_t p47 = (p45 & 0xFFFFFF00u) | (p67 & ~0xFFFFFF00u);
+    uint32_t t = (p03 & 0xFFFF0000u) | (p47 & 0x0000FFFFu);
+    // two variable shifts with fillers: t <<= sh; t |= bbs & array_shift[sh]
     b.y[2] = barrett_sq(b.y[2], b.nM[2], b.mu[2]);
-    sh = b.y[2] & 3u;
-    t <<= sh;
+    uint32_t sh = b.y[2] & 3u;
     b.y[0] = barrett_sq(b.y[0], b.nM[0], b.mu[0]);
-    t |= b.y[0] & ((1u << sh) - 1u);
+    t = (t << sh) | (b.y[0] & low_mask(sh));
     b.y[6] = barrett_sq(b.y[6], b.nM[6], b.mu[6]);
     sh = b.y[6] & 3u;
-    t <<= sh;
     b.y[1] = barrett_sq(b.y[1], b.nM[1], b.mu[1]);
-    t |= b.y[1] & ((1u << sh) - 1u);
+    t = (t << sh) | (b.y[1] & low_mask(sh));
     return t;
 }
 
@@ -60,6 +76,7 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     uint32_t *P = a.state;
     const uint64_t L = a.n_local;
+    const uint4 *modtab = reinterpret_cast<const uint4 *>(a.mod);
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += warps) {
@@ -67,14 +84,14 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         const bool valid = row < a.s_count;
         const uint64_t s = a.s_begin + row;
         Bbs8 b;
-        uint32_t m[8];
         uint32_t x = 0, tp = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             b.y[j] = valid ? P[j * L + s] : 2u;
-            m[j] = valid ? P[(8 + j) * L + s] : 0u;
-            b.nM[j] = 0u - __ldg(a.mod + 2 * m[j]);
-            b.mu[j] = __ldg(a.mod + 2 * m[j] + 1);
+            const uint32_t m = valid ? P[(8 + j) * L + s] : 0u;
+            const uint4 e = __ldg(modtab + m);  // {M, mu, 2^32 - M, 0}
+            b.mu[j] = e.y;
+            b.nM[j] = e.z;
         }
         if (valid) {
             x = P[16 * L + s];
@@ -96,7 +113,14 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
             sink.put4(0, i, o0, o1, o2, o3, valid);
         }
         for (; i < a.n; ++i) sink.put1(0, i, round(), valid);
+        sink.end_rows(valid ? 1u : 0u);
         if (valid && a.n > 0) {
+            // rotation (Q19): instance j moves to slot j+1 with its modulus
+            // index, which is re-read from the untouched call-entry plane
+            // instead of being held in 8 registers through the loop
+            uint32_t m[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) m[j] = P[(8 + j) * L + s];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 P[((j + 1) & 7) * L + s] = b.y[j];

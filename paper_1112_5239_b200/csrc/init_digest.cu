@@ -58,12 +58,37 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
             for (int k = 0; k < 4; ++k) P[k * L + r] = g[k];
             P[4 * L + r] = (uint32_t)seed_word(a.seed, s, 4);
             P[5 * L + r] = (uint32_t)seed_word(a.seed, s, 5);
+        } else if (a.variant == 3) {
+            // V3 (NEXT-1): xor64 a = W(s,0) (0 -> Marsaglia seed), x, tp
+            uint64_t w0 = seed_word(a.seed, s, 0);
+            if (w0 == 0) w0 = 88172645463325252ull;
+            P[0 * L + r] = (uint32_t)w0;
+            P[1 * L + r] = (uint32_t)(w0 >> 32);
+            P[2 * L + r] = (uint32_t)seed_word(a.seed, s, 1);
+            P[3 * L + r] = (uint32_t)seed_word(a.seed, s, 2);
+        } else if (a.variant == 4) {
+            // V4 (NEXT-1): V0's generator words, x = W(s,11), tp = W(s,12)
+            uint64_t w[11];
+            for (int k = 0; k < 11; ++k) w[k] = seed_word(a.seed, s, k);
+            if (w[0] == 0) w[0] = 88172645463325252ull;
+            if ((w[1] | w[2] | w[3] | w[4]) == 0) {
+                w[1] = 123456789u; w[2] = 362436069u; w[3] = 521288629u; w[4] = 88675123u;
+            }
+            if ((w[5] | w[6] | w[7] | w[8] | w[9]) == 0) {
+                w[5] = 123456789u; w[6] = 362436069u; w[7] = 521288629u; w[8] = 88675123u; w[9] = 5783321u;
+            }
+            for (int k = 0; k < 11; ++k) {
+                P[(2 * k) * L + r] = (uint32_t)w[k];
+                P[(2 * k + 1) * L + r] = (uint32_t)(w[k] >> 32);
+            }
+            P[22 * L + r] = (uint32_t)seed_word(a.seed, s, 11);
+            P[23 * L + r] = (uint32_t)seed_word(a.seed, s, 12);
         } else {
             // Q21: y = r^2 mod M, gcd(r, M) = 1, y not in {0, 1}
             for (int j = 0; j < 8; ++j) {
                 const uint64_t w = seed_word(a.seed, s, j);
                 const uint32_t mi = (uint32_t)(w >> 32) % a.n_mod;
-                const uint32_t M = a.mod[2 * mi];
+                const uint32_t M = a.mod[4 * mi];
                 uint32_t rr = 2u + (uint32_t)w % (M - 3u);
                 while (gcd_u32(rr, M) != 1u || (rr * rr) % M <= 1u) rr = (rr == M - 2u) ? 2u : rr + 1u;
                 P[j * L + r] = (rr * rr) % M;

@@ -37,7 +37,7 @@ struct InitArgs {
     uint64_t first_stream;
     int variant;
     int paper_defaults;
-    const uint32_t *mod;  // V2: [n_mod][2] = {M, mu}
+    const uint32_t *mod;  // V2: [n_mod][4] = {M, mu, 2^32 - M, 0}
     uint32_t n_mod;
 };
 
@@ -58,6 +58,9 @@ int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               int persistent_blocks, const V1Tuning &tune);
 int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
+int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
+              int persistent_blocks);
+int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);
 

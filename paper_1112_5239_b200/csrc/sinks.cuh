@@ -35,6 +35,7 @@ struct StoreSink {
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
         if (valid) base[slot][i] = o;
     }
+    __device__ __forceinline__ void end_rows(uint32_t) {}
     __device__ __forceinline__ void finish(const GenArgs &) {}
     static constexpr int kSmemBytesPerWarp = 0;
     static constexpr bool kStats = false;
@@ -42,47 +43,76 @@ struct StoreSink {
 
 // Consumer statistics (reading Q24): per-warp 256-bin shared-memory
 // histogram of x >> 24, per-lane count of Monte-Carlo pi pairs
-// (x_{2k}, x_{2k+1}) inside the quarter disc.  Flushed once per CTA into the
+// (x_{2k}, x_{2k+1}) OUTSIDE the quarter disc.  Flushed once per CTA into the
 // caller's u64 stats[258] with global atomics (integer sums: order-free).
+//
+// Issue economy (the consumer is integer-issue bound, ncu r1c: ALU pipe 84 %):
+//  * a pair is outside iff u^2 + v^2 carries out of 64 bits, so the test is
+//    two IMAD.WIDE (FMA pipe) and a three-instruction carry chain whose last
+//    add-with-carry IS the counter update (no compare, no select);
+//  * the bin's byte offset (x >> 24) * 4 is one IMAD.HI plus one LOP3;
+//  * pair counts are not counted per pair: end_rows() adds n/2 per valid row,
+//    and inside = pairs - outside at the end.
+__device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_t v) {
+    asm("{\n\t"
+        ".reg .u64 U, V;\n\t"
+        ".reg .u32 ul, uh, vl, vh, d;\n\t"
+        "mul.wide.u32 U, %1, %1;\n\t"
+        "mul.wide.u32 V, %2, %2;\n\t"
+        "mov.b64 {ul, uh}, U;\n\t"
+        "mov.b64 {vl, vh}, V;\n\t"
+        "add.cc.u32 d, ul, vl;\n\t"
+        "addc.cc.u32 d, uh, vh;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "}"
+        : "+r"(cnt)
+        : "r"(u), "r"(v));
+}
+
 struct StatsSink {
-    uint32_t *hist;      // this warp's 256 bins
-    uint64_t inside;     // this lane's count
-    uint32_t inside32;   // fast accumulator, folded into `inside`
+    uint32_t hist;       // shared address of this warp's 256 u32 bins
+    uint32_t out32;      // outside pairs since the last end_rows (< 2^31, host-checked n)
+    uint64_t outside;    // this lane's outside pairs
+    uint64_t pairs;      // this lane's valid pairs
     uint32_t pend[2];    // stashed even-round value for put1 tails, per stream slot
-    uint64_t pairs;      // valid pairs seen by this lane
     uint64_t n;
     __device__ __forceinline__ explicit StatsSink(const GenArgs &a)
-        : inside(0), inside32(0), pend{0, 0}, pairs(0), n(a.n) {
+        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n) {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
         for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
         __syncthreads();
-        hist = all + 256u * (threadIdx.x >> 5);
+        hist = smem_u32(all) + 1024u * (threadIdx.x >> 5);
+    }
+    __device__ __forceinline__ void bin(uint32_t o) {
+        const uint32_t off = shr_fma<22>(o) & 0x3FCu;  // (o >> 24) * 4
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist + off) : "memory");
     }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool valid) {
         if (!valid) return;
-        atomicAdd(&hist[o0 >> 24], 1u);
-        atomicAdd(&hist[o1 >> 24], 1u);
-        atomicAdd(&hist[o2 >> 24], 1u);
-        atomicAdd(&hist[o3 >> 24], 1u);
-        inside32 += pi_inside(o0, o1) + pi_inside(o2, o3);
-        pairs += 2;
-        if (inside32 >= 0x80000000u) { inside += inside32; inside32 = 0; }
+        bin(o0);
+        bin(o1);
+        bin(o2);
+        bin(o3);
+        count_outside(out32, o0, o1);
+        count_outside(out32, o2, o3);
     }
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
         if (!valid) return;
-        atomicAdd(&hist[o >> 24], 1u);
-        if (i & 1) {
-            inside32 += pi_inside(pend[slot], o);
-            pairs += 1;
-        } else {
-            pend[slot] = o;
-        }
+        bin(o);
+        if (i & 1) count_outside(out32, pend[slot], o);
+        else pend[slot] = o;
+    }
+    // after the rounds of a tile: this lane owned `rows` valid streams
+    __device__ __forceinline__ void end_rows(uint32_t rows) {
+        outside += out32;
+        out32 = 0;
+        pairs += (uint64_t)rows * (n >> 1);
     }
     __device__ void finish(const GenArgs &a) {
-        uint64_t v = inside + inside32, p = pairs;
+        uint64_t v = pairs - outside, p = pairs;
 #pragma unroll
         for (int d = 16; d; d >>= 1) {
             v += __shfl_xor_sync(kFull, v, d);
@@ -92,7 +122,7 @@ struct StatsSink {
         uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
         const uint32_t nw = blockDim.x >> 5;
         __syncthreads();
-        // fold warp histograms into warp 0's copy, then one atomic per bin
+        // fold warp histograms, then one atomic per bin per CTA
         for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) {
             uint32_t acc = 0;
             for (uint32_t w = 0; w < nw; ++w) acc += all[256u * w + b];

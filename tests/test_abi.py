@@ -53,7 +53,9 @@ def _create(seed, first, n_local, variant, comb_size=0, comb=None, paper_default
 @pytest.mark.parametrize(
     "args",
     [
-        dict(seed=0, first=0, n_local=32, variant=3),                     # unknown variant
+        dict(seed=0, first=0, n_local=32, variant=5),                     # unknown variant
+        dict(seed=0, first=0, n_local=33, variant=3),                     # V3: incomplete group
+        dict(seed=0, first=0, n_local=4, variant=4, comb_size=4),         # V4: defaults need C = 32
         dict(seed=0, first=0, n_local=0, variant=1),                      # no streams
         dict(seed=0, first=0, n_local=33, variant=1),                     # incomplete group
         dict(seed=0, first=16, n_local=32, variant=1),                    # misaligned shard

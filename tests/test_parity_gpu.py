@@ -148,8 +148,42 @@ def test_v1_hand_trace_injected(golden):
     assert P.as_u32(g.generate(3)).tolist() == e["outputs"]
 
 
+# ------------------------------------------------------------------ V3 / V4
+# NEXT-1: Alg. 4 with the xor64 source (V3, Q29) and with
+# Listing 1's fold (V4, Q30); same arrays, exchange and store paths as V1.
+@pytest.mark.parametrize("seed", SEEDS)
+@pytest.mark.parametrize("S", [32, 64, 96, 4096])
+@pytest.mark.parametrize("store_path", [P.STORE_DIRECT, P.STORE_TMA])
+def test_v3_default_tables(seed, S, store_path):
+    info = _check(W.V3, seed, S, NS, store_path=store_path)
+    assert info.kernel_launches == 1
+
+
+@pytest.mark.parametrize("variant", [W.V3, W.V4])
+@pytest.mark.parametrize("C", [1, 2, 8, 32])
+def test_v34_custom_tables(variant, C):
+    comb = W.random_comb(W.rng(200 + C), C, 2)
+    for S in (C * 3 if C < 32 else 64, 512):
+        _check(variant, SEEDS[1], S, [5, 64, 3], comb_size=C, comb=comb)
+
+
+@pytest.mark.parametrize("seed", SEEDS)
+@pytest.mark.parametrize("S", [32, 96, 1024])
+def test_v4_default_tables(seed, S):
+    _check(W.V4, seed, S, [0, 1, 3, 4, 19, 20, 21, 100, 5])
+
+
+@pytest.mark.parametrize("variant", [W.V3, W.V4])
+def test_v34_misaligned_and_shards(variant):
+    _check(variant, 3, 128, [8, 12], out_offset_words=1)
+    whole, _, _ = gpu_run(variant, SEEDS[0], 1024, [40])
+    hi, _, _ = gpu_run(variant, SEEDS[0], 512, [40], first=512)
+    assert np.array_equal(whole[0][512:], hi[0])
+
+
 # ------------------------------------------------------------------ consumer
-@pytest.mark.parametrize("variant,S,n", [(W.V0, 100, 38), (W.V1, 2048, 130), (W.V1, 96, 6), (W.V2, 1024, 66)])
+@pytest.mark.parametrize("variant,S,n", [(W.V0, 100, 38), (W.V1, 2048, 130), (W.V1, 96, 6), (W.V2, 1024, 66),
+                                         (W.V3, 2048, 130), (W.V3, 96, 6), (W.V4, 256, 42)])
 def test_consume_matches_oracle_stats(variant, S, n):
     g = P.ChaoticPRNG(SEEDS[0], S, variant)
     stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
@@ -174,6 +208,8 @@ def test_consume_custom_tables_and_odd_n():
     assert np.array_equal(P.as_u64(stats), ref)
     with pytest.raises(P.PrngError):
         g.consume(3)
+    with pytest.raises(P.PrngError):  # per-lane u32 pair counters: n < 2^31 per call
+        g.consume(2**31)
 
 
 # -------------------------------------------------------------------- digest
@@ -245,7 +281,7 @@ def test_gpu_output_statistics():
         assert 1e-4 < statcheck.hist_chi2_p(s[2:]) < 1 - 1e-4
 
 
-@pytest.mark.parametrize("cols,wpb,grid,persist", [(8, 2, 0, 0), (32, 8, 0, 0), (16, 4, 1, 0), (32, 2, 3, 0),
+@pytest.mark.parametrize("cols,wpb,grid,persist", [(8, 2, 0, 0), (32, 8, 0, 0), (16, 4, 1, 0), (32, 2, 3, 0), (32, 2, 1, 0),
                                                    (8, 8, 1, 0), (64, 1, 0, 0), (64, 2, 0, -1), (128, 1, 0, 0),
                                                    (128, 2, 0, -1), (128, 1, 0, 2)])
 def test_v1_store_kernel_shapes(monkeypatch, cols, wpb, grid, persist):

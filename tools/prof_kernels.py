@@ -1,5 +1,5 @@
 """Small driver for ncu captures: a few calls of one workload through the
-C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|consume} [calls]"""
+C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|v3|v4|consume} [calls]"""
 import os
 import sys
 
@@ -27,6 +27,12 @@ elif which == "v2":
 elif which == "v0":
     S, n = 2**20, 128
     g = P.ChaoticPRNG(seed, S, P.V0)
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+elif which in ("v3", "v4"):
+    S, n = 2**20, 128
+    g = P.ChaoticPRNG(seed, S, P.V3 if which == "v3" else P.V4)
     out = torch.empty((S, n), dtype=torch.int32, device="cuda")
     for _ in range(calls):
         g.generate(n, out=out)
