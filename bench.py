@@ -215,26 +215,51 @@ def run_ours(args):
     store_path_used = g.info().store_path
     torch.cuda.synchronize()
 
+    # (1) headline: L2 flushed between timed steps (a 256 MiB write > the 126
+    # MB L2 before every call, outside the timed interval), each call timed
+    # with CUDA events on the launching stream -- the state planes (24 MiB)
+    # start every call in HBM.
+    scratch = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(lr) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        # back-to-back launches (no per-launch events: they would break the
-        # programmatic-dependent-launch overlap between consecutive kernels)
         for k in range(args.steps):
+            scratch.fill_(k)
+            ev[k][0].record(stream)
             g.generate(n, out=out)
-        t_end.record(stream)
+            ev[k][1].record(stream)
         torch.cuda.synchronize()
     barrier()
-    total_ms = t_start.elapsed_time(t_end)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     numbers = args.steps * S * n * ws
     value = numbers / (total_ms / 1e3)
+    del scratch
+
+    # (2) steady state: back-to-back calls with no flush (no per-launch events:
+    # they would break the programmatic-dependent-launch overlap).  The output
+    # is stored L2-evict-first, so across calls the state planes stay
+    # L2-resident -- the regime of a generator serving calls continuously.
+    barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        g.generate(n, out=out)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    steady_ms = t_start.elapsed_time(t_end)
+    t = torch.tensor([steady_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    steady_ms = float(t.item())
+    steady_value = numbers / (steady_ms / 1e3)
 
     # ---- end-to-end through the public API with a pinned host buffer
     host = torch.empty((S, n), dtype=torch.int32, pin_memory=True)
@@ -254,8 +279,7 @@ def run_ours(args):
     # ---- roofline of the dominant (only) kernel
     peak, peak_src, peaks = measured_peaks()
     alg_bytes = 4 * S * n + 2 * STATE_BYTES_V1 * S
-    # every launch in the timed region is this one kernel: its average launch
-    # duration is the region time / K (inter-launch gaps included)
+    # every timed interval holds exactly one launch of this one kernel
     avg_kern_s = total_ms / args.steps / 1e3
     achieved = alg_bytes / avg_kern_s / 1e9
     traffic = ncu_traffic()
@@ -286,7 +310,8 @@ def run_ours(args):
             "n_per_stream": n,
             "global_streams": S * ws,
             "store_path": {1: "direct", 2: "tma"}.get(store_path_used, str(store_path_used)),
-            "l2": f"output {4 * S * n >> 20} MiB per step per GPU > 126 MB L2 (inputs larger than L2, no flush)",
+            "l2": "L2 flushed before every timed step (256 MiB write, untimed); output "
+                  f"{4 * S * n >> 20} MiB per step per GPU, state {STATE_BYTES_V1 * S >> 20} MiB",
             "parallelism": f"stream-sharded x{ws} (no collective on the store path)",
         },
         "roofline": {
@@ -309,6 +334,14 @@ def run_ours(args):
             "api": "prng_generate_host (pinned host buffer, chunked generate + D2H overlap)",
             "steps": e2e_steps,
         },
+        "steady_state": {
+            "value": steady_value,
+            "unit": UNIT,
+            "ms_per_step": steady_ms / args.steps,
+            "frac": alg_bytes / (steady_ms / args.steps / 1e3) / 1e9 / peak,
+            "note": "back-to-back calls, no L2 flush: output stored evict-first, so the 24 MiB of state "
+                    "planes stay L2-resident across calls (only the output reaches HBM)",
+        },
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
@@ -330,17 +363,21 @@ def measure_secondary(P, torch, dev, args):
     res = {}
     stream = torch.cuda.current_stream()
 
+    scratch = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
+
     def timed(fn, steps):
+        """mean seconds per call; L2 flushed (untimed) before every call."""
         for _ in range(3):
             fn()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         torch.cuda.synchronize()
-        a.record(stream)
-        for _ in range(steps):
+        for k in range(steps):
+            scratch.fill_(k)
+            ev[k][0].record(stream)
             fn()
-        b.record(stream)
+            ev[k][1].record(stream)
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / 1e3 / steps
+        return sum(a.elapsed_time(b) for a, b in ev) / 1e3 / steps
 
     S, n = W.CONFIGS["C3"]["n_streams"], W.CONFIGS["C3"]["n"]
     g = P.ChaoticPRNG(W.SEEDS[0], S, P.V2)
@@ -368,6 +405,33 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: g.consume(n5, stats), 10)
     res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
     g.close()
+    from paper_1112_5239_b200 import battery as B
+
+    g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
+    bstats = torch.zeros(P.N_BATTERY, dtype=torch.int64, device=dev)
+    s = timed(lambda: g.battery(n5, bstats), 10)
+    pv = B.pvalues(P.as_u64(bstats), S5 * 13, n5)  # 3 warm-up + 10 timed calls
+    res["v1_battery"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5,
+                         "numbers_tested": S5 * n5 * 13, "pvalues": pv, "pass_1e-4": B.passes(pv)}
+    g.close()
+    # NEXT-3: batch chaotic Blum-Goldwasser encryption, 2^18 messages x 1024
+    # units, moduli ~2^62 (a pool of 256 seeded Blum-prime keys), r < p, q
+    from paper_1112_5239_b200 import bg as BGm
+
+    import numpy as np
+
+    gen = W.rng(99)
+    keys = W.bg_keys(gen, 256, 31)
+    Bm, Lm = 2**18, 1024
+    Ns = np.array([keys[k % 256][2] for k in range(Bm)], dtype=np.uint64)
+    rs = gen.integers(2, 2**30, Bm).astype(np.uint64)
+    Nt = torch.from_numpy(Ns.view(np.int64)).to(dev)
+    rt = torch.from_numpy(rs.view(np.int64)).to(dev)
+    S0 = torch.from_numpy(gen.integers(0, 32, Bm).astype(np.int32)).to(dev)
+    msg = torch.randint(0, 256, (Bm, Lm), dtype=torch.uint8, device=dev)
+    s = timed(lambda: BGm.encrypt(True, Nt, rt, msg, S0), 10)
+    res["cbg_encrypt"] = {"value": Bm * Lm / s, "unit": "keystream units/s", "ms_per_call": s * 1e3,
+                          "messages": Bm, "units_per_message": Lm, "modulus_bits": 62, "unit_bits": 5}
     return res
 
 

@@ -168,8 +168,26 @@ CIPRNG_API int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *ou
  * Integer sums, so results are independent of launch shape and of how
  * streams are sharded (the multi-GPU all-reduce is bit-exact).
  * Errors: PRNG_EINVAL if n is odd or a pointer is NULL, PRNG_ESIZE if
- * n >= 2^31 (split the call; V0/V1 are split invariant), PRNG_ECUDA. */
+ * n >= 2^24 (split the call; V0/V1/V3/V4 are split invariant), PRNG_ECUDA. */
 CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
+
+/* Statistical battery in consumer form (the tests of
+ * monobit, block frequency m = 128, runs, serial 2-bit,
+ * byte chi-square, 8-lag autocorrelation -- stand in for the BigCrush runs
+ * the paper reports).  Runs the same n rounds as prng_generate
+ * (identical state evolution) and ADDS integer counts into stats_dev[264]
+ * (u64, caller-zeroed).  A stream's bit sequence within the call is its
+ * words in round order, each most significant bit first (reading Q31):
+ *   [0] one bits            [1] adjacent bit pairs that differ
+ *   [2] adjacent pairs 11   [3] bit pairs 8 apart that differ
+ *   [4] sum over 128-bit blocks (words 4k..4k+3) of (ones - 64)^2
+ *   [5] number of blocks    [6] / [7] first / last bits equal to 1
+ *   [8 + b] bytes equal to b, all four bytes of every word.
+ * P-values are computed on the host from these counts
+ * (paper_1112_5239_b200/battery.py).  Integer sums: independent of launch
+ * shape and sharding.  Errors: PRNG_EINVAL (NULL), PRNG_ESIZE (n >= 2^20),
+ * PRNG_ECUDA. */
+CIPRNG_API int prng_battery(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
 
 /* Verification digest of one call's output block (reading Q28):
  * digest_dev[0] += sum over s < n_local, i < n of
@@ -177,6 +195,46 @@ CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_de
  * mix64 = SplitMix64 finaliser.  Position-aware and additive across shards. */
 CIPRNG_API int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n,
                 uint64_t *digest_dev, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Blum-Goldwasser and the paper's chaotic variant  */
+/* ---------------------------------------------------------------------- */
+
+/* Batch encryption, one independent message per GPU thread.
+ * Classic Blum-Goldwasser (chaotic == 0): x_0 = r^2 mod N,
+ * c_i = m_i ^ lsb(x_i), x_{i+1} = x_i^2 mod N, y = x_L.
+ * Chaotic variant (chaotic != 0, reading Q33): units of
+ * Nb = floor(log2(log2 N)) bits, b_i = x_i mod 2^Nb,
+ * c_i = m_i ^ (b_0 ^ ... ^ b_i) ^ S0 (the cumulative XOR of Eq. "Oplus").
+ * Arguments (device pointers, caller-owned):
+ *   N_dev[n_msgs]  public moduli, odd, 3 <= N < 2^63 (N = p q, p, q = 3 mod 4)
+ *   S0_dev[n_msgs] the variant's public S0 (< 2^Nb); NULL = all 0; ignored
+ *                  by classic BG
+ *   r_dev[n_msgs]  the sender's random r, gcd(r, N) = 1
+ *   m_dev, c_dev   L units per message, one unit per byte (a bit for
+ *                  classic BG, Nb bits for the variant; higher bits of m are
+ *                  ignored, those of c are 0), message-major: unit i of
+ *                  message k at [k * L + i]
+ *   y_dev[n_msgs]  out: y = x_L mod N.  A message whose N or r
+ *                  violates the constraints gets y = 0 (never a valid y) and
+ *                  no ciphertext.
+ * Enqueued on `stream`.  Errors: PRNG_EINVAL (NULL pointers), PRNG_ESIZE,
+ * PRNG_ECUDA. */
+CIPRNG_API int prng_cbg_encrypt(int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *N_dev,
+                                const uint32_t *S0_dev, const uint64_t *r_dev, const uint8_t *m_dev,
+                                uint8_t *c_dev, uint64_t *y_dev, void *stream);
+
+/* Batch decryption with the secret factors: r_p =
+ * y^(((p+1)/4)^L) mod p, r_q likewise, x_0 = q (q^-1 mod p) r_p +
+ * p (p^-1 mod q) r_q mod N, then the same keystream as encryption (for the
+ * variant the cumulative one: reading Q33 -- the paper's "same decryption
+ * stage leads to m_i ^ S0" omits the cumulative terms).
+ * p_dev, q_dev: primes = 3 (mod 4), p != q, p q < 2^63; c_dev, y_dev as
+ * produced by prng_cbg_encrypt; m_dev out.  status_dev (may be NULL): 0 ok,
+ * 1 invalid key or y >= N (no plaintext written). */
+CIPRNG_API int prng_cbg_decrypt(int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *p_dev,
+                                const uint64_t *q_dev, const uint32_t *S0_dev, const uint8_t *c_dev,
+                                const uint64_t *y_dev, uint8_t *m_dev, uint32_t *status_dev, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Introspection, checkpoint / test hooks                                 */

@@ -60,6 +60,15 @@ def lib():
         L.orc_grid_generate.restype = i32
         L.orc_stats_words.argtypes, L.orc_stats_words.restype = [vp, u64, u64, vp], i32
         L.orc_digest_words.argtypes, L.orc_digest_words.restype = [vp, u64, u64, u64], u64
+        L.orc_battery_words.argtypes, L.orc_battery_words.restype = [vp, u64, u64, vp], i32
+        L.orc_modmul.argtypes, L.orc_modmul.restype = [u64, u64, u64], u64
+        L.orc_modpow.argtypes, L.orc_modpow.restype = [u64, u64, u64], u64
+        L.orc_modinv.argtypes, L.orc_modinv.restype = [u64, u64, vp], i32
+        L.orc_bg_unit_bits.argtypes, L.orc_bg_unit_bits.restype = [u64], u32
+        L.orc_cbg_encrypt.argtypes = [i32, u64, u32, u64, u64, vp, vp, vp]
+        L.orc_cbg_encrypt.restype = i32
+        L.orc_cbg_decrypt.argtypes = [i32, u64, u64, u32, u64, vp, u64, vp]
+        L.orc_cbg_decrypt.restype = i32
         _lib = L
     return _lib
 
@@ -158,6 +167,53 @@ def stats(words: np.ndarray, acc: np.ndarray | None = None) -> np.ndarray:
     if rc != 0:
         raise OracleError(f"orc_stats_words rc={rc}")
     return acc
+
+
+N_BATTERY = 264
+
+
+def battery(words: np.ndarray, acc: np.ndarray | None = None) -> np.ndarray:
+    """264 u64 battery counts of a (n_local, n) block of one call (reading Q31)."""
+    words = np.ascontiguousarray(words, dtype=np.uint32)
+    acc = np.zeros(N_BATTERY, dtype=np.uint64) if acc is None else acc
+    rc = lib().orc_battery_words(_ptr(words), words.shape[0], words.shape[1], _ptr(acc))
+    if rc != 0:
+        raise OracleError(f"orc_battery_words rc={rc}")
+    return acc
+
+
+# ------------------------------------------------- Blum-Goldwasser (NEXT-3)
+def modpow(a: int, e: int, m: int) -> int:
+    return lib().orc_modpow(a, e, m)
+
+
+def modinv(a: int, m: int) -> int:
+    out = np.zeros(1, np.uint64)
+    if lib().orc_modinv(a, m, _ptr(out)) != 0:
+        raise OracleError("not invertible")
+    return int(out[0])
+
+
+def bg_unit_bits(N: int) -> int:
+    return lib().orc_bg_unit_bits(N)
+
+
+def cbg_encrypt(chaotic: bool, N: int, S0: int, r: int, m) -> tuple[np.ndarray, int]:
+    """(c units, y); classic BG when chaotic is False (units = bits)."""
+    m = np.ascontiguousarray(m, dtype=np.uint8)
+    c = np.zeros_like(m)
+    y = np.zeros(1, np.uint64)
+    if lib().orc_cbg_encrypt(int(chaotic), N, S0, r, m.size, _ptr(m), _ptr(c), _ptr(y)) != 0:
+        raise OracleError("cbg_encrypt: invalid key or r")
+    return c, int(y[0])
+
+
+def cbg_decrypt(chaotic: bool, p: int, q: int, S0: int, c, y: int) -> np.ndarray:
+    c = np.ascontiguousarray(c, dtype=np.uint8)
+    m = np.zeros_like(c)
+    if lib().orc_cbg_decrypt(int(chaotic), p, q, S0, c.size, _ptr(c), y, _ptr(m)) != 0:
+        raise OracleError("cbg_decrypt: invalid key or ciphertext")
+    return m
 
 
 def digest(words: np.ndarray, first_stream: int = 0) -> int:

@@ -617,6 +617,171 @@ int orc_stats_words(const uint32_t *out, uint64_t n_local, uint64_t n, uint64_t 
     return ORC_OK;
 }
 
+/* ======================================================================== */
+/* Statistical battery counts (monobit, */
+/* block frequency m = 128, runs, serial 2-bit, byte chi-square, 8-lag       */
+/* autocorrelation -- the desk-scale stand-in for the BigCrush runs of       */
+/* P:851-853).  Reading Q31: the bit sequence of a stream within one call is  */
+/* its words x_0 .. x_{n-1} in round order, each word most significant bit   */
+/* first; sequences never continue across streams or calls.  Plain bit-by-  */
+/* bit loops.  Accumulated (u64) into stats[264]:                            */
+/*   [0] ones            [1] adjacent pairs that differ   [2] adjacent 11    */
+/*   [3] pairs 8 apart that differ   [4] sum over 128-bit blocks (4 words at */
+/*   round index 4k..4k+3) of (ones in block - 64)^2   [5] number of blocks  */
+/*   [6] first bits equal to 1   [7] last bits equal to 1                    */
+/*   [8 + b] bytes equal to b over all four bytes of every word              */
+/* ======================================================================== */
+#define ORC_BATTERY_WORDS 264
+
+static uint32_t bit_at(const uint32_t *w, uint64_t j) /* j-th bit, MSB first */
+{
+    return (w[j / 32] >> (31u - (uint32_t)(j % 32))) & 1u;
+}
+
+int orc_battery_words(const uint32_t *out, uint64_t n_local, uint64_t n, uint64_t *stats)
+{
+    uint64_t s, j, k;
+    for (s = 0; s < n_local; s++) {
+        const uint32_t *w = out + s * n;
+        uint64_t N = 32u * n;
+        if (n == 0) continue;
+        for (j = 0; j < N; j++) {
+            uint32_t b = bit_at(w, j);
+            stats[0] += b;
+            if (j + 1 < N) {
+                uint32_t c = bit_at(w, j + 1);
+                stats[1] += (b != c);
+                stats[2] += (b == 1u && c == 1u);
+            }
+            if (j + 8 < N) stats[3] += (b != bit_at(w, j + 8));
+        }
+        for (k = 0; k + 4 <= n; k += 4) {
+            int64_t ones = 0, d;
+            for (j = 32u * k; j < 32u * (k + 4); j++) ones += bit_at(w, j);
+            d = ones - 64;
+            stats[4] += (uint64_t)(d * d);
+            stats[5] += 1;
+        }
+        stats[6] += bit_at(w, 0);
+        stats[7] += bit_at(w, N - 1);
+        for (k = 0; k < n; k++) {
+            stats[8 + (w[k] & 0xFFu)] += 1;
+            stats[8 + ((w[k] >> 8) & 0xFFu)] += 1;
+            stats[8 + ((w[k] >> 16) & 0xFFu)] += 1;
+            stats[8 + (w[k] >> 24)] += 1;
+        }
+    }
+    return ORC_OK;
+}
+
+/* ======================================================================== */
+/* NEXT-3: Blum-Goldwasser and the paper's chaotic variant     */
+/* (P:1368-1386), on moduli N < 2^63 (unsigned __int128 products).           */
+/* Units are one byte each: bits for classic BG (b_i = lsb x_i),     */
+/* blocks of Nb = floor(log2(log2 N)) bits for the variant (P:1371-1372;     */
+/* reading Q33: b_i = x_i mod 2^Nb, c_i = m_i ^ (b_0 ^ .. ^ b_i) ^ S0,       */
+/* decryption with the same cumulative keystream).                          */
+/* ======================================================================== */
+uint64_t orc_modmul(uint64_t a, uint64_t b, uint64_t m)
+{
+    return (uint64_t)(((unsigned __int128)a * b) % m);
+}
+
+uint64_t orc_modpow(uint64_t a, uint64_t e, uint64_t m)
+{
+    uint64_t r = 1 % m;
+    a %= m;
+    while (e) {
+        if (e & 1u) r = orc_modmul(r, a, m);
+        a = orc_modmul(a, a, m);
+        e >>= 1;
+    }
+    return r;
+}
+
+/* extended Euclid; ORC_EINVAL if gcd(a, m) != 1 */
+int orc_modinv(uint64_t a, uint64_t m, uint64_t *inv)
+{
+    __int128 t = 0, nt = 1, r = (__int128)m, nr = (__int128)(a % m), q, tmp;
+    while (nr != 0) {
+        q = r / nr;
+        tmp = t - q * nt; t = nt; nt = tmp;
+        tmp = r - q * nr; r = nr; nr = tmp;
+    }
+    if (r != 1) return ORC_EINVAL;
+    if (t < 0) t += (__int128)m;
+    *inv = (uint64_t)t;
+    return ORC_OK;
+}
+
+static uint64_t gcd64(uint64_t a, uint64_t b)
+{
+    while (b) { uint64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+/* Nb = floor(log2(log2 N)) = the largest t with N >= 2^(2^t). */
+uint32_t orc_bg_unit_bits(uint64_t N)
+{
+    uint32_t t = 0;
+    /* 2^(2^(t+1)) for t + 1 <= 5 fits in 64 bits; N < 2^63 < 2^(2^6) */
+    while (t < 5 && N >= (1ull << (1u << (t + 1)))) t++;
+    return t;
+}
+
+/* chaotic != 0: the variant; else classic BG.  m, c: L units.  Returns
+ * ORC_EINVAL if N is even, N < 3, N >= 2^63 or gcd(r, N) != 1 (the paper's
+ * r in [1, N] must be a unit, else it leaks a factor). */
+int orc_cbg_encrypt(int chaotic, uint64_t N, uint32_t S0, uint64_t r, uint64_t L, const uint8_t *m, uint8_t *c,
+                    uint64_t *y)
+{
+    uint64_t x, i;
+    uint32_t Nb = orc_bg_unit_bits(N), mask = (1u << Nb) - 1u, B = 0;
+    if (N < 3 || !(N & 1u) || (N >> 63) || gcd64(r % N, N) != 1) return ORC_EINVAL;
+    x = orc_modmul(r, r, N);                       /* x_0 = r^2 mod N */
+    for (i = 0; i < L; i++) {
+        if (chaotic) {
+            B ^= (uint32_t)(x & mask);                 /* b_0 ^ ... ^ b_i */
+            c[i] = (uint8_t)((m[i] ^ B ^ S0) & mask);
+        } else {
+            c[i] = (uint8_t)((m[i] ^ (uint32_t)(x & 1u)) & 1u);  /* lsb of x_i */
+        }
+        x = orc_modmul(x, x, N);                   /* x_{i+1} = x_i^2 mod N */
+    }
+    *y = x;                                        /* y = x_0^(2^L) mod N */
+    return ORC_OK;
+}
+
+/* Decryption: r_p = y^(((p+1)/4)^L) mod p, r_q likewise,
+ * x_0 = q (q^-1 mod p) r_p + p (p^-1 mod q) r_q mod N, regenerate the
+ * keystream.  Exponents are reduced mod p-1 (Fermat). */
+int orc_cbg_decrypt(int chaotic, uint64_t p, uint64_t q, uint32_t S0, uint64_t L, const uint8_t *c, uint64_t y,
+                    uint8_t *m)
+{
+    uint64_t N = p * q, ep, eq, rp, rq, ip, iq, x, i;
+    uint32_t Nb, mask, B = 0;
+    if (p < 3 || q < 3 || p == q || (p & 3u) != 3u || (q & 3u) != 3u) return ORC_EINVAL;
+    if ((unsigned __int128)p * q >= ((unsigned __int128)1 << 63) || y >= N) return ORC_EINVAL;
+    if (orc_modinv(q % p, p, &iq) || orc_modinv(p % q, q, &ip)) return ORC_EINVAL;
+    ep = orc_modpow((p + 1) / 4, L, p - 1);
+    eq = orc_modpow((q + 1) / 4, L, q - 1);
+    rp = orc_modpow(y % p, ep, p);
+    rq = orc_modpow(y % q, eq, q);
+    x = (orc_modmul(orc_modmul(q, iq, N), rp, N) + orc_modmul(orc_modmul(p, ip, N), rq, N)) % N;
+    Nb = orc_bg_unit_bits(N);
+    mask = (1u << Nb) - 1u;
+    for (i = 0; i < L; i++) {
+        if (chaotic) {
+            B ^= (uint32_t)(x & mask);
+            m[i] = (uint8_t)((c[i] ^ B ^ S0) & mask);
+        } else {
+            m[i] = (uint8_t)((c[i] ^ (uint32_t)(x & 1u)) & 1u);
+        }
+        x = orc_modmul(x, x, N);
+    }
+    return ORC_OK;
+}
+
 /* Verification digest (reading Q28): sum over the call's words of
  * mix64(mix64(idx) ^ x_idx) mod 2^64, idx = (first_stream + s) * n + i. */
 uint64_t orc_digest_words(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n)

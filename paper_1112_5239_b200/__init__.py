@@ -30,8 +30,10 @@ from ._lib import (  # noqa: F401
 V0, V1, V2, V3, V4 = 0, 1, 2, 3, 4
 STATE_WORDS = {V0: 23, V1: 6, V2: 18, V3: 4, V4: 24}
 N_STATS = 258
+N_BATTERY = 264
 
-__all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "V3", "V4", "STATE_WORDS", "N_STATS", "lib", "PrngError"]
+__all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "V3", "V4", "STATE_WORDS", "N_STATS", "N_BATTERY", "lib",
+           "PrngError"]
 
 
 def _stream_handle(stream) -> ctypes.c_void_p:
@@ -99,6 +101,16 @@ class ChaoticPRNG:
         assert stats.is_cuda and stats.numel() == N_STATS and stats.dtype == torch.int64
         check(lib().prng_consume(self._h, n, ctypes.c_void_p(stats.data_ptr()), _stream_handle(stream)),
               "prng_consume")
+        return stats
+
+    def battery(self, n: int, stats: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Statistical-battery counts (include/ciprng.h prng_battery): adds into
+        int64 [264] (u64 bits).  P-values: ``battery.pvalues``."""
+        if stats is None:
+            stats = torch.zeros(N_BATTERY, dtype=torch.int64, device=self.device)
+        assert stats.is_cuda and stats.numel() == N_BATTERY and stats.dtype == torch.int64
+        check(lib().prng_battery(self._h, n, ctypes.c_void_p(stats.data_ptr()), _stream_handle(stream)),
+              "prng_battery")
         return stats
 
     # ------------------------------------------------------------ introspection

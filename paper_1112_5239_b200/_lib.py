@@ -68,6 +68,9 @@ def lib() -> ctypes.CDLL:
             "prng_generate": ([vp, u64, vp, vp], i32),
             "prng_generate_host": ([vp, u64, vp, vp], i32),
             "prng_consume": ([vp, u64, vp, vp], i32),
+            "prng_battery": ([vp, u64, vp, vp], i32),
+            "prng_cbg_encrypt": ([i32, u64, u64, vp, vp, vp, vp, vp, vp, vp], i32),
+            "prng_cbg_decrypt": ([i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, vp], i32),
             "prng_digest": ([vp, u64, u64, u64, vp, vp], i32),
             "prng_get_info": ([vp, ctypes.POINTER(PrngInfo)], i32),
             "prng_get_state": ([vp, vp, sz], i32),

@@ -91,6 +91,14 @@ constexpr int kStateWords[5] = {23, 6, 18, 4, 24};
 
 }  // namespace
 
+thread_local ciprng::L2Window ciprng::g_l2win;
+
+static bool env_on(const char *name, bool dflt) {
+    const char *v = std::getenv(name);
+    if (!v || !v[0]) return dflt;
+    return v[0] != '0';
+}
+
 bool ciprng::pdl_enabled() {
     static const bool on = [] {
         const char *v = std::getenv("CIPRNG_PDL");
@@ -112,6 +120,13 @@ struct prng_s {
     uint32_t n_mod = 0;
     int num_sms = 148;
     int persistent_blocks = 0;
+    // Evict-first output stores (default; CIPRNG_EVICT_FIRST=0 disables) and an
+    // optional persisting-L2 window over the state planes (CIPRNG_L2PERSIST=1;
+    // measured slower than evict-first alone on B200, gpurun_out/s11).
+    size_t l2win_bytes = 0;
+    float l2win_hit = 0.f;
+    bool evict_first = true;
+    bool state_last = true;
     V1Tuning v1tune;
     // last call info
     int last_path = 0;
@@ -193,6 +208,16 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
     a.C = h->C;
     a.comb = h->comb;
     a.vec = (out != nullptr && (n % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0)) ? 1u : 0u;
+    a.evict_first = h->evict_first ? 1u : 0u;
+    a.state_last = h->state_last ? 1u : 0u;
+    struct WindowScope {  // the state's L2 access-policy window for this pass's launches
+        explicit WindowScope(const prng_t *hh) {
+            g_l2win.base = hh->l2win_bytes ? hh->state : nullptr;
+            g_l2win.bytes = hh->l2win_bytes;
+            g_l2win.hit = hh->l2win_hit;
+        }
+        ~WindowScope() { g_l2win = L2Window(); }
+    } window_scope(h);
     int launches = 0;
     int path = PRNG_STORE_DIRECT;
     if (h->variant == 0) {
@@ -331,6 +356,32 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         delete h;
         return PRNG_ENOMEM;
     }
+    h->evict_first = env_on("CIPRNG_EVICT_FIRST", true);
+    {
+        // evict-last only pays while the planes are a small part of L2 (V1 24
+        // MiB, V3 16 MiB at 2^20 streams); for V0/V2/V4's 72-96 MiB it evicts
+        // useful lines (measured: V2 -11 %, gpurun_out/r1f)
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
+        h->state_last = env_on("CIPRNG_STATE_EVICT_LAST", true) && l2 > 0 && words * 4 <= (size_t)l2 / 4;
+    }
+    if (env_on("CIPRNG_L2PERSIST", false)) {
+        // persisting-L2 carve-out (device-wide limit; only ever raised) sized
+        // to the state planes, and a launch window covering them
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+        if (max_persist > 0 && max_window > 0) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t want = std::min(words * 4, (size_t)max_persist);
+            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            h->l2win_bytes = std::min(words * 4, (size_t)max_window);
+            h->l2win_hit = h->l2win_bytes ? std::min(1.0f, (float)cur / (float)h->l2win_bytes) : 0.f;
+        }
+        cudaGetLastError();  // the policy is an optimisation: never fail creation on it
+    }
     std::vector<uint32_t> tab = modulus_table();
     h->n_mod = (uint32_t)(tab.size() / 4);
     e = cudaMalloc(&h->mod, tab.size() * 4);
@@ -457,9 +508,18 @@ int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *st
     if (!h || !stats_dev || (n_per_stream & 1)) return PRNG_EINVAL;
     h->last_launches = 0;
     if (n_per_stream == 0) return PRNG_OK;
-    if (n_per_stream >= (1ull << 31)) return PRNG_ESIZE;  // per-lane u32 pair counters
+    if (n_per_stream >= (1ull << 24)) return PRNG_ESIZE;  // u32 tile counters (sinks.cuh)
     DeviceGuard g(h->device);
     return run_pass(h, n_per_stream, 0, h->n_local, nullptr, stats_dev, 2, (cudaStream_t)stream);
+}
+
+int prng_battery(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream) {
+    if (!h || !stats_dev) return PRNG_EINVAL;
+    h->last_launches = 0;
+    if (n_per_stream == 0) return PRNG_OK;
+    if (n_per_stream >= (1ull << 20)) return PRNG_ESIZE;  // u32 tile counters (sinks.cuh)
+    DeviceGuard g(h->device);
+    return run_pass(h, n_per_stream, 0, h->n_local, nullptr, stats_dev, 3, (cudaStream_t)stream);
 }
 
 int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest_dev,
@@ -469,6 +529,28 @@ int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     launch_digest(out_dev, first_stream, n_local, n, digest_dev, (cudaStream_t)stream, sms * 8);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
+}
+
+int prng_cbg_encrypt(int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *N_dev, const uint32_t *S0_dev,
+                     const uint64_t *r_dev, const uint8_t *m_dev, uint8_t *c_dev, uint64_t *y_dev, void *stream) {
+    if (n_msgs == 0) return PRNG_OK;
+    if (!N_dev || !r_dev || !y_dev || (L && (!m_dev || !c_dev))) return PRNG_EINVAL;
+    if (L && n_msgs > SIZE_MAX / L) return PRNG_ESIZE;
+    launch_cbg(true, chaotic, n_msgs, L, N_dev, r_dev, S0_dev, m_dev, c_dev, y_dev, nullptr, (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
+}
+
+int prng_cbg_decrypt(int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *p_dev, const uint64_t *q_dev,
+                     const uint32_t *S0_dev, const uint8_t *c_dev, const uint64_t *y_dev, uint8_t *m_dev,
+                     uint32_t *status_dev, void *stream) {
+    if (n_msgs == 0) return PRNG_OK;
+    if (!p_dev || !q_dev || !y_dev || (L && (!m_dev || !c_dev))) return PRNG_EINVAL;
+    if (L && n_msgs > SIZE_MAX / L) return PRNG_ESIZE;
+    launch_cbg(false, chaotic, n_msgs, L, p_dev, q_dev, S0_dev, c_dev, m_dev, const_cast<uint64_t *>(y_dev),
+               status_dev, (cudaStream_t)stream);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
 }

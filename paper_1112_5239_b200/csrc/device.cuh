@@ -92,6 +92,11 @@ __device__ __forceinline__ void st_v4(uint32_t *p, uint32_t a, uint32_t b, uint3
     asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
+// streaming (evict-first) variant: the output is written once, never re-read
+__device__ __forceinline__ void st_v4_cs(uint32_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -107,6 +112,37 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t sm
         "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
             reinterpret_cast<uint64_t>(map)),
         "r"(smem_addr), "r"(c0), "r"(c1)
+        : "memory");
+}
+// Same with an L2 cache-eviction policy (createpolicy): the output is written
+// once and never re-read by this kernel, so it is stored evict-first and does
+// not push the L2-persisting state planes out.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// State-plane accesses with an L2 policy (evict-last keeps the planes, read
+// and rewritten every call, resident while the output streams through L2).
+__device__ __forceinline__ uint32_t ld_state(const uint32_t *p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_state(uint32_t *p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap *map, uint32_t smem_addr, int c0, int c1,
+                                                  uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_addr), "r"(c0), "r"(c1), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -165,7 +201,29 @@ struct GenArgs {
     const uint32_t *mod; // V2: [78][4] = {M, mu, 2^32 - M, 0}
     uint32_t C;          // combination_size
     uint32_t vec;        // 1: rows are 16-byte aligned, n % 4 == 0
+    uint32_t evict_first; // 1: output stores carry an L2 evict-first hint
+    uint32_t state_last;  // 1: state-plane loads/stores carry an L2 evict-last hint
     CombTables comb;
+};
+
+// SoA state-plane access (plane k of local stream s at word k*L + s) with the
+// evict-last L2 hint when enabled (a.state_last).
+struct StateIO {
+    uint32_t *P;
+    uint64_t L;
+    uint64_t pol;
+    bool last;
+    __device__ __forceinline__ explicit StateIO(const GenArgs &a)
+        : P(a.state), L(a.n_local), pol(l2_evict_last_policy()), last(a.state_last != 0) {}
+    __device__ __forceinline__ uint32_t ld(uint32_t k, uint64_t s) const {
+        const uint32_t *p = P + k * L + s;
+        return last ? ld_state(p, pol) : *p;
+    }
+    __device__ __forceinline__ void st(uint32_t k, uint64_t s, uint32_t v) const {
+        uint32_t *p = P + k * L + s;
+        if (last) st_state(p, v, pol);
+        else *p = v;
+    }
 };
 
 }  // namespace ciprng

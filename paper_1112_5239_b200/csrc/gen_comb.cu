@@ -26,13 +26,13 @@ namespace ciprng {
 struct SrcXor64 {
     static constexpr int kPlanes = 2;  // a.lo, a.hi; then x, tp
     u64p a;
-    __device__ __forceinline__ void load(const uint32_t *P, uint64_t L, uint64_t s) {
-        a.lo = P[0 * L + s];
-        a.hi = P[1 * L + s];
+    __device__ __forceinline__ void load(const StateIO &io, uint64_t s) {
+        a.lo = io.ld(0, s);
+        a.hi = io.ld(1, s);
     }
-    __device__ __forceinline__ void store(uint32_t *P, uint64_t L, uint64_t s) const {
-        P[0 * L + s] = a.lo;
-        P[1 * L + s] = a.hi;
+    __device__ __forceinline__ void store(const StateIO &io, uint64_t s) const {
+        io.st(0, s, a.lo);
+        io.st(1, s, a.hi);
     }
     __device__ __forceinline__ void zero() { a = {0u, 0u}; }
     __device__ __forceinline__ uint32_t next() {
@@ -55,8 +55,7 @@ __global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
     const uint32_t src2 = gbase + a.comb.t[1][off];
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += warps) {
@@ -67,9 +66,9 @@ __global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
         uint32_t x = 0, tp = 0;
         g.zero();
         if (valid) {
-            g.load(P, L, s);
-            x = P[X * L + s];
-            tp = P[TP * L + s];
+            g.load(sio, s);
+            x = sio.ld(X, s);
+            tp = sio.ld(TP, s);
         }
         sink.begin_row(0, row);
         auto round = [&]() -> uint32_t {
@@ -86,9 +85,9 @@ __global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
         for (; i < a.n; ++i) sink.put1(0, i, round(), valid);
         sink.end_rows(valid ? 1u : 0u);
         if (valid) {
-            g.store(P, L, s);
-            P[X * L + s] = x;
-            P[TP * L + s] = tp;
+            g.store(sio, s);
+            sio.st(X, s, x);
+            sio.st(TP, s, tp);
         }
     }
     sink.finish(a);
@@ -110,8 +109,7 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
     const uint32_t src = (j + 1u) & 15u;
     const uint64_t n_tiles = (a.s_count + kCombTileRows - 1) / kCombTileRows;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
     const uint32_t rA_t = 32u * h + j, rB_t = rA_t + 16u;
 
     uint32_t wsmem = 0;
@@ -133,10 +131,10 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
         gA.zero();
         gB.zero();
         if (valid) {
-            gA.load(P, L, sA);
-            gB.load(P, L, sB);
-            xA = P[X * L + sA]; tpA = P[TP * L + sA];
-            xB = P[X * L + sB]; tpB = P[TP * L + sB];
+            gA.load(sio, sA);
+            gB.load(sio, sB);
+            xA = sio.ld(X, sA); tpA = sio.ld(TP, sA);
+            xB = sio.ld(X, sB); tpB = sio.ld(TP, sB);
         }
         sink.begin_row(0, rA);
         sink.begin_row(1, rB);
@@ -175,7 +173,8 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tmap, buf, (int)i0, (int)row0);
+                    if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
+                    else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
                     bulk_commit();
                 }
                 ++issued;
@@ -204,10 +203,10 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
                 tpA = lastA ^ nb;
                 tpB = lastB ^ nb;
             }
-            gA.store(P, L, sA);
-            gB.store(P, L, sB);
-            P[X * L + sA] = xA; P[TP * L + sA] = tpA;
-            P[X * L + sB] = xB; P[TP * L + sB] = tpB;
+            gA.store(sio, sA);
+            gB.store(sio, sB);
+            sio.st(X, sA, xA); sio.st(TP, sA, tpA);
+            sio.st(X, sB, xB); sio.st(TP, sB, tpB);
         }
     }
     if constexpr (kTma) {
@@ -227,7 +226,7 @@ static int comb_blocks(uint64_t warps_needed, int wpb, int cap) {
 template <class Src>
 static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
                        int persistent_blocks) {
-    // mode: 0 store-direct, 1 store-tma, 2 consume
+    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
     if (a.s_count == 0) return 0;
     CUtensorMap dummy;
     if (tmap == nullptr) tmap = &dummy;
@@ -241,9 +240,12 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
             launch_k(kern, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), smem, st, a, *tmap);
         } else if (mode == 0) {
             launch_k(comb_fast_kernel<Src, StoreSink, 0>, dim3(comb_blocks(tiles, 4, 0)), dim3(128), 0, st, a, *tmap);
-        } else {
+        } else if (mode == 2) {
             launch_k(comb_fast_kernel<Src, StatsSink, 0>, dim3(comb_blocks(tiles, 4, persistent_blocks)), dim3(128),
                      4 * StatsSink::kSmemBytesPerWarp, st, a, *tmap);
+        } else {
+            launch_k(comb_fast_kernel<Src, BatterySink, 0>, dim3(comb_blocks(tiles, 4, persistent_blocks)), dim3(128),
+                     4 * BatterySink::kSmemBytesPerWarp, st, a, *tmap);
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;
@@ -251,6 +253,9 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
         if (mode == 2) {
             launch_k(comb_general_kernel<Src, StatsSink>, dim3(comb_blocks(tiles, wpb, persistent_blocks)),
                      dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+        } else if (mode == 3) {
+            launch_k(comb_general_kernel<Src, BatterySink>, dim3(comb_blocks(tiles, wpb, persistent_blocks)),
+                     dim3(32 * wpb), wpb * BatterySink::kSmemBytesPerWarp, st, a);
         } else {
             launch_k(comb_general_kernel<Src, StoreSink>, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), 0, st, a);
         }

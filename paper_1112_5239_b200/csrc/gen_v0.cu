@@ -35,8 +35,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
     const uint32_t src1 = gbase + a.comb.t[0][off], src2 = gbase + a.comb.t[1][off];
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += warps) {
@@ -46,7 +45,7 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
         uint64_t ra = 0, rb[4] = {0, 0, 0, 0}, rc[5] = {0, 0, 0, 0, 0}, rd = 0;
         uint32_t x = 0, tp = 0;
         auto ld64 = [&](int k) -> uint64_t {
-            return (uint64_t)P[(2 * k) * L + s] | ((uint64_t)P[(2 * k + 1) * L + s] << 32);
+            return (uint64_t)sio.ld(2 * k, s) | ((uint64_t)sio.ld(2 * k + 1, s) << 32);
         };
         if (valid) {
             ra = ld64(0);
@@ -55,8 +54,8 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
 #pragma unroll
             for (int k = 0; k < 5; ++k) rc[k] = ld64(5 + k);
             rd = ld64(10);
-            x = P[22 * L + s];
-            if (kComb) tp = P[23 * L + s];
+            x = sio.ld(22, s);
+            if (kComb) tp = sio.ld(23, s);
         }
         // x ^= f (V0), or Alg. 4's combination with f as the source (V4)
         auto update = [&](uint32_t f) {
@@ -118,8 +117,8 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
         sink.end_rows(valid ? 1u : 0u);
         if (valid) {
             auto st64 = [&](int k, uint64_t v) {
-                P[(2 * k) * L + s] = (uint32_t)v;
-                P[(2 * k + 1) * L + s] = (uint32_t)(v >> 32);
+                sio.st(2 * k, s, (uint32_t)v);
+                sio.st(2 * k + 1, s, (uint32_t)(v >> 32));
             };
             st64(0, ra);
 #pragma unroll
@@ -127,8 +126,8 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
 #pragma unroll
             for (int k = 0; k < 5; ++k) st64(5 + k, rc[k]);
             st64(10, rd);
-            P[22 * L + s] = x;
-            if (kComb) P[23 * L + s] = tp;
+            sio.st(22, s, x);
+            if (kComb) sio.st(23, s, tp);
         }
     }
     sink.finish(a);
@@ -144,6 +143,10 @@ static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st, int persisten
         if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
         launch_k(v0_kernel<StatsSink, kComb>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp,
                  st, a);
+    } else if (mode == 3) {
+        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
+        launch_k(v0_kernel<BatterySink, kComb>, dim3((int)blocks), dim3(32 * wpb),
+                 wpb * BatterySink::kSmemBytesPerWarp, st, a);
     } else {
         launch_k(v0_kernel<StoreSink, kComb>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }

@@ -38,8 +38,7 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
     const uint32_t src2 = gbase + a.comb.t[1][off];
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
          tile += warps) {
@@ -48,8 +47,8 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
         const uint64_t s = a.s_begin + row;
         uint32_t g0 = 0, g1 = 0, g2 = 0, g3 = 0, x = 0, tp = 0;
         if (valid) {
-            g0 = P[0 * L + s]; g1 = P[1 * L + s]; g2 = P[2 * L + s]; g3 = P[3 * L + s];
-            x = P[4 * L + s]; tp = P[5 * L + s];
+            g0 = sio.ld(0, s); g1 = sio.ld(1, s); g2 = sio.ld(2, s); g3 = sio.ld(3, s);
+            x = sio.ld(4, s); tp = sio.ld(5, s);
         }
         sink.begin_row(0, row);
         uint64_t i = 0;
@@ -78,8 +77,8 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
         }
         sink.end_rows(valid ? 1u : 0u);
         if (valid) {
-            P[0 * L + s] = g0; P[1 * L + s] = g1; P[2 * L + s] = g2; P[3 * L + s] = g3;
-            P[4 * L + s] = x; P[5 * L + s] = tp;
+            sio.st(0, s, g0); sio.st(1, s, g1); sio.st(2, s, g2); sio.st(3, s, g3);
+            sio.st(4, s, x); sio.st(5, s, tp);
         }
     }
     sink.finish(a);
@@ -124,13 +123,14 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
     // all warp stall samples when every tile waited for its own loads).
     uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     uint32_t pa[6] = {0, 0, 0, 0, 0, 0}, pb[6] = {0, 0, 0, 0, 0, 0};
+    const StateIO sio(a);
     auto prefetch = [&](uint64_t t) {
         if (t < n_tiles && t * kFastTileRows + 32u * h < a.s_count) {
             const uint64_t sA = a.s_begin + t * kFastTileRows + rA_t, sB = sA + 16u;
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
-                pa[k] = P[k * L + sA];
-                pb[k] = P[k * L + sB];
+                pa[k] = sio.ld(k, sA);
+                pb[k] = sio.ld(k, sB);
             }
         }
     };
@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tmap, buf, (int)i0, (int)row0);
+                    if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
+                    else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
                     bulk_commit();
                 }
                 ++tma_issued;
@@ -223,10 +224,12 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                 tpA = a3 ^ nb;
                 tpB = b3 ^ nb;
             }
-            P[0 * L + sA] = a0; P[1 * L + sA] = a1; P[2 * L + sA] = a2; P[3 * L + sA] = a3;
-            P[4 * L + sA] = xA; P[5 * L + sA] = tpA;
-            P[0 * L + sB] = b0; P[1 * L + sB] = b1; P[2 * L + sB] = b2; P[3 * L + sB] = b3;
-            P[4 * L + sB] = xB; P[5 * L + sB] = tpB;
+            const uint32_t vA[6] = {a0, a1, a2, a3, xA, tpA}, vB[6] = {b0, b1, b2, b3, xB, tpB};
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                sio.st(k, sA, vA[k]);
+                sio.st(k, sB, vB[k]);
+            }
         }
     }
     if constexpr (kTma) {
@@ -393,7 +396,7 @@ static void launch_fast_tma(const GenArgs &a, const CUtensorMap &tm, int grid, i
 
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               int persistent_blocks, const V1Tuning &tune) {
-    // mode: 0 store-direct, 1 store-tma, 2 consume
+    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
     if (a.s_count == 0) return 0;
     if (fast) {
         const uint64_t tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
@@ -402,7 +405,7 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
         CUtensorMap dummy;
         if (tmap == nullptr) tmap = &dummy;
         if (mode == 0) {
-            v1_fast_kernel<StoreSink, 0><<<blocks_for(tiles, wpb, cap), 32 * wpb, 0, st>>>(a, *tmap);
+            launch_k(v1_fast_kernel<StoreSink, 0>, dim3(blocks_for(tiles, wpb, cap)), dim3(32 * wpb), 0, st, a, *tmap);
         } else if (mode == 1) {
             const int grid = blocks_for(tiles, wpb, cap);
             if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
@@ -412,7 +415,12 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             else launch_fast_tma<16>(a, *tmap, grid, wpb, st);
         } else {
             int grid = blocks_for(tiles, 4, persistent_blocks);
-            launch_k(v1_fast_kernel<StatsSink, 0>, dim3(grid), dim3(128), 4 * StatsSink::kSmemBytesPerWarp, st, a, *tmap);
+            if (mode == 3)
+                launch_k(v1_fast_kernel<BatterySink, 0>, dim3(grid), dim3(128), 4 * BatterySink::kSmemBytesPerWarp, st,
+                         a, *tmap);
+            else
+                launch_k(v1_fast_kernel<StatsSink, 0>, dim3(grid), dim3(128), 4 * StatsSink::kSmemBytesPerWarp, st, a,
+                         *tmap);
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;
@@ -420,6 +428,10 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
         if (mode == 2) {
             int grid = blocks_for(tiles, wpb, persistent_blocks);
             launch_k(v1_general_kernel<StatsSink>, dim3(grid), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+        } else if (mode == 3) {
+            int grid = blocks_for(tiles, wpb, persistent_blocks);
+            launch_k(v1_general_kernel<BatterySink>, dim3(grid), dim3(32 * wpb), wpb * BatterySink::kSmemBytesPerWarp,
+                     st, a);
         } else {
             int grid = blocks_for(tiles, wpb, 0);
             launch_k(v1_general_kernel<StoreSink>, dim3(grid), dim3(32 * wpb), 0, st, a);

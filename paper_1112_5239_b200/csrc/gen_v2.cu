@@ -74,8 +74,7 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     const uint32_t off = lane % C, gbase = lane - off;
     const uint64_t n_tiles = (a.s_count + 31) / 32;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
     const uint4 *modtab = reinterpret_cast<const uint4 *>(a.mod);
 
     for (uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < n_tiles;
@@ -87,15 +86,15 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         uint32_t x = 0, tp = 0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            b.y[j] = valid ? P[j * L + s] : 2u;
-            const uint32_t m = valid ? P[(8 + j) * L + s] : 0u;
+            b.y[j] = valid ? sio.ld(j, s) : 2u;
+            const uint32_t m = valid ? sio.ld(8 + j, s) : 0u;
             const uint4 e = __ldg(modtab + m);  // {M, mu, 2^32 - M, 0}
             b.mu[j] = e.y;
             b.nM[j] = e.z;
         }
         if (valid) {
-            x = P[16 * L + s];
-            tp = P[17 * L + s];
+            x = sio.ld(16, s);
+            tp = sio.ld(17, s);
         }
         const uint32_t src1 = gbase + a.comb.t[b.y[0] & 7u][off];
         const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
@@ -120,14 +119,14 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
             // instead of being held in 8 registers through the loop
             uint32_t m[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) m[j] = P[(8 + j) * L + s];
+            for (int j = 0; j < 8; ++j) m[j] = sio.ld(8 + j, s);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                P[((j + 1) & 7) * L + s] = b.y[j];
-                P[(8 + ((j + 1) & 7)) * L + s] = m[j];
+                sio.st((j + 1) & 7, s, b.y[j]);
+                sio.st(8 + ((j + 1) & 7), s, m[j]);
             }
-            P[16 * L + s] = x;
-            P[17 * L + s] = tp;
+            sio.st(16, s, x);
+            sio.st(17, s, tp);
         }
     }
     sink.finish(a);
@@ -141,6 +140,10 @@ int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks
     if (mode == 2) {
         if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
         launch_k(v2_kernel<StatsSink>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+    } else if (mode == 3) {
+        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
+        launch_k(v2_kernel<BatterySink>, dim3((int)blocks), dim3(32 * wpb), wpb * BatterySink::kSmemBytesPerWarp, st,
+                 a);
     } else {
         launch_k(v2_kernel<StoreSink>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }

@@ -11,6 +11,18 @@ namespace ciprng {
 
 struct GenArgs;
 
+// L2 residency of the handle's state planes (set by api.cu around each
+// launch): the state is read and written once per call (48 B/stream for V1)
+// while the output streams past it, so it is marked persisting in L2 and the
+// output is written evict-first -- across back-to-back calls the state then
+// never travels to HBM.  base == nullptr: no window.
+struct L2Window {
+    void *base = nullptr;
+    size_t bytes = 0;
+    float hit = 0.f;  // fraction of the window that may persist (carve-out / window)
+};
+extern thread_local L2Window g_l2win;
+
 // Launch with programmatic stream serialization (see device.cuh pdl_wait);
 // falls back to a plain launch when disabled (CIPRNG_PDL=0).
 bool pdl_enabled();
@@ -22,11 +34,24 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    unsigned na = 0;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (g_l2win.base != nullptr) {
+        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[na].val.accessPolicyWindow.base_ptr = g_l2win.base;
+        at[na].val.accessPolicyWindow.num_bytes = g_l2win.bytes;
+        at[na].val.accessPolicyWindow.hitRatio = g_l2win.hit;
+        at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -61,6 +86,8 @@ int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks
 int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               int persistent_blocks);
 int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
+int launch_cbg(bool encrypt, int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *a0, const uint64_t *a1,
+               const uint32_t *S0, const uint8_t *in, uint8_t *out, uint64_t *y, uint32_t *status, cudaStream_t st);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);
 

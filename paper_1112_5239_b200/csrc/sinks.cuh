@@ -14,9 +14,10 @@ namespace ciprng {
 struct StoreSink {
     uint32_t *out;
     uint64_t n;
-    bool vec;
+    bool vec, cs;       // cs: L2 evict-first (streaming) stores
     uint32_t *base[2];  // row start of each of the lane's (up to two) streams
-    __device__ __forceinline__ explicit StoreSink(const GenArgs &a) : out(a.out), n(a.n), vec(a.vec != 0) {}
+    __device__ __forceinline__ explicit StoreSink(const GenArgs &a)
+        : out(a.out), n(a.n), vec(a.vec != 0), cs(a.evict_first != 0) {}
     // slot: which of the lane's streams (the V1 fast kernel owns two)
     __device__ __forceinline__ void begin_row(int slot, uint64_t row) { base[slot] = out + row * n; }
     __device__ __forceinline__ void put4(int slot, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2,
@@ -24,16 +25,19 @@ struct StoreSink {
         if (!valid) return;
         uint32_t *p = base[slot] + i;
         if (vec) {
-            st_v4(p, o0, o1, o2, o3);
+            if (cs) st_v4_cs(p, o0, o1, o2, o3);
+            else st_v4(p, o0, o1, o2, o3);
         } else {
-            p[0] = o0;
-            p[1] = o1;
-            p[2] = o2;
-            p[3] = o3;
+            put1(slot, i, o0, true);
+            put1(slot, i + 1, o1, true);
+            put1(slot, i + 2, o2, true);
+            put1(slot, i + 3, o3, true);
         }
     }
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
-        if (valid) base[slot][i] = o;
+        if (!valid) return;
+        if (cs) __stcs(base[slot] + i, o);
+        else base[slot][i] = o;
     }
     __device__ __forceinline__ void end_rows(uint32_t) {}
     __device__ __forceinline__ void finish(const GenArgs &) {}
@@ -53,6 +57,28 @@ struct StoreSink {
 //  * the bin's byte offset (x >> 24) * 4 is one IMAD.HI plus one LOP3;
 //  * pair counts are not counted per pair: end_rows() adds n/2 per valid row,
 //    and inside = pairs - outside at the end.
+// Flush a warp's 256-bin u32 shared histogram into u64 global counters and
+// zero it (all 32 lanes call it together).  The sinks call it whenever the
+// increments since the last flush could reach 2^31, so the u32 bins never
+// wrap whatever the data.
+__device__ __forceinline__ void warp_hist_flush(uint32_t hist, uint64_t *gdst) {
+    __syncwarp();
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t addr = hist + 4u * (8u * lane + k);
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+        if (v) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(gdst + 8u * lane + k), (unsigned long long)v);
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(0u) : "memory");
+        }
+    }
+    __syncwarp();
+}
+constexpr uint64_t kHistFlushAt = 1ull << 31;
+constexpr uint64_t kMaxRowsPerWarpTile = 64;  // the fast kernels' tile; others use 32
+
 __device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_t v) {
     asm("{\n\t"
         ".reg .u64 U, V;\n\t"
@@ -76,8 +102,10 @@ struct StatsSink {
     uint64_t pairs;      // this lane's valid pairs
     uint32_t pend[2];    // stashed even-round value for put1 tails, per stream slot
     uint64_t n;
+    uint64_t pending;    // bin increments of this warp since its last flush (upper bound)
+    uint64_t *gstats;
     __device__ __forceinline__ explicit StatsSink(const GenArgs &a)
-        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n) {
+        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n), pending(0), gstats(a.stats) {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
         for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
@@ -110,6 +138,11 @@ struct StatsSink {
         outside += out32;
         out32 = 0;
         pairs += (uint64_t)rows * (n >> 1);
+        pending += kMaxRowsPerWarpTile * n;
+        if (pending + kMaxRowsPerWarpTile * n >= kHistFlushAt) {  // warp-uniform
+            warp_hist_flush(hist, gstats + 2);
+            pending = 0;
+        }
     }
     __device__ void finish(const GenArgs &a) {
         uint64_t v = pairs - outside, p = pairs;
@@ -131,6 +164,112 @@ struct StatsSink {
         if ((threadIdx.x & 31) == 0) {
             if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 0), (unsigned long long)v);
             if (p) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 1), (unsigned long long)p);
+        }
+    }
+    static constexpr int kSmemBytesPerWarp = 1024;
+    static constexpr bool kStats = true;
+};
+
+// Statistical battery counts (reading
+// Q31: a stream's bit sequence within one call is its words in round order,
+// each most significant bit first).  Same state evolution as StatsSink; per
+// word the lane adds into u32 tile accumulators (folded into u64 by
+// end_rows; the host caps n < 2^20 so they cannot wrap):
+//   ones, adjacent differing pairs, adjacent 11 pairs, pairs 8 apart that
+//   differ (the cross-word terms use the previous word of the same stream),
+//   sum over 4-word blocks of (ones - 64)^2; the first / last bit of each
+//   stream; and a per-warp shared histogram of all four bytes of every word.
+// stats layout (264 u64): [0] ones [1] diff [2] c11 [3] lag8 [4] block_sq
+// [5] blocks [6] first ones [7] last ones [8 + b] byte b.
+struct BatterySink {
+    static constexpr int kWords = 264;
+    uint32_t hist;           // shared address of this warp's 256 u32 bins
+    uint32_t ones, diff, c11, lag8, bsq;
+    uint64_t acc[8];
+    uint32_t prev[2];
+    uint64_t n;
+    uint64_t pending;
+    uint64_t *gstats;
+    __device__ __forceinline__ explicit BatterySink(const GenArgs &a)
+        : ones(0), diff(0), c11(0), lag8(0), bsq(0), acc{0, 0, 0, 0, 0, 0, 0, 0}, prev{0, 0}, n(a.n), pending(0),
+          gstats(a.stats) {
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
+        for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
+        __syncthreads();
+        hist = smem_u32(all) + 1024u * (threadIdx.x >> 5);
+    }
+    __device__ __forceinline__ void bin(uint32_t b) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist + 4u * b) : "memory");
+    }
+    // one word x of a stream whose previous word in this call is p (has_prev)
+    __device__ __forceinline__ void word(uint32_t x, uint32_t p, bool has_prev) {
+        ones += __popc(x);
+        diff += __popc((x ^ (x >> 1)) & 0x7FFFFFFFu);
+        c11 += __popc(x & (x >> 1));
+        lag8 += __popc((x ^ (x >> 8)) & 0x00FFFFFFu);
+        if (has_prev) {
+            diff += (p ^ (x >> 31)) & 1u;
+            c11 += p & (x >> 31) & 1u;
+            lag8 += __popc((p ^ (x >> 24)) & 0xFFu);
+        }
+        bin(x & 0xFFu);
+        bin((x >> 8) & 0xFFu);
+        bin((x >> 16) & 0xFFu);
+        bin(x >> 24);
+    }
+    __device__ __forceinline__ void begin_row(int, uint64_t) {}
+    __device__ __forceinline__ void put4(int slot, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
+                                         bool valid) {
+        if (!valid) return;
+        if (i == 0) acc[6] += o0 >> 31;
+        word(o0, prev[slot], i != 0);
+        word(o1, o0, true);
+        word(o2, o1, true);
+        word(o3, o2, true);
+        const int c = (int)(__popc(o0) + __popc(o1) + __popc(o2) + __popc(o3)) - 64;
+        bsq += (uint32_t)(c * c);
+        prev[slot] = o3;
+    }
+    __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
+        if (!valid) return;
+        if (i == 0) acc[6] += o >> 31;
+        word(o, prev[slot], i != 0);
+        prev[slot] = o;
+    }
+    __device__ __forceinline__ void end_rows(uint32_t rows) {
+        acc[0] += ones; acc[1] += diff; acc[2] += c11; acc[3] += lag8; acc[4] += bsq;
+        ones = diff = c11 = lag8 = bsq = 0;
+        acc[5] += (uint64_t)rows * (n >> 2);
+        if (rows >= 1) acc[7] += prev[0] & 1u;
+        if (rows >= 2) acc[7] += prev[1] & 1u;
+        pending += 4 * kMaxRowsPerWarpTile * n;
+        if (pending + 4 * kMaxRowsPerWarpTile * n >= kHistFlushAt) {  // warp-uniform
+            warp_hist_flush(hist, gstats + 8);
+            pending = 0;
+        }
+    }
+    __device__ void finish(const GenArgs &a) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint64_t v = acc[k];
+#pragma unroll
+            for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+            acc[k] = v;
+        }
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
+        const uint32_t nw = blockDim.x >> 5;
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) {
+            uint64_t s = 0;
+            for (uint32_t w = 0; w < nw; ++w) s += all[256u * w + b];
+            if (s) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 8 + b), (unsigned long long)s);
+        }
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (acc[k]) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + k), (unsigned long long)acc[k]);
         }
     }
     static constexpr int kSmemBytesPerWarp = 1024;

@@ -296,3 +296,40 @@ def test_v1_store_kernel_shapes(monkeypatch, cols, wpb, grid, persist):
     monkeypatch.setenv("CIPRNG_V1_PERSIST", str(persist))
     for S in (96, 4096 + 32, 65536):
         _check(W.V1, SEEDS[0], S, [4, 36, 128, 20, 96, 160, 256], store_path=P.STORE_TMA)
+
+
+# ------------------------------------------------------------------ battery
+# NEXT-2: on-device statistical battery counts == oracle counts
+# (integer, bit-exact), then the >= 10^10-numbers-per-variant run of the
+# SURVEY row, judged by the host p-values.
+@pytest.mark.parametrize("variant,S,n", [(W.V0, 100, 38), (W.V1, 2048, 130), (W.V1, 96, 7), (W.V2, 1024, 66),
+                                         (W.V3, 2048, 128), (W.V3, 96, 5), (W.V4, 256, 42)])
+def test_battery_matches_oracle_counts(variant, S, n):
+    g = P.ChaoticPRNG(SEEDS[2], S, variant)
+    stats = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        g.battery(n, stats)
+    got = P.as_u64(stats)
+    st = O.init_states(variant, SEEDS[2], 0, S)
+    ref = np.zeros(O.N_BATTERY, np.uint64)
+    for _ in range(2):
+        O.battery(O.generate(variant, st, n), ref)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+    with pytest.raises(P.PrngError):
+        g.battery(2**20)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", [W.V0, W.V1, W.V2, W.V3, W.V4])
+def test_battery_1e10_numbers(variant):
+    from paper_1112_5239_b200 import battery as B
+
+    S, n = 2**20, 1024
+    calls = -(-10**10 // (S * n))  # >= 1e10 numbers
+    g = P.ChaoticPRNG(SEEDS[0], S, variant)
+    stats = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    for _ in range(calls):
+        g.battery(n, stats)
+    p = B.pvalues(P.as_u64(stats), S * calls, n)
+    assert B.passes(p, alpha=1e-4), p

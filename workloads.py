@@ -42,3 +42,49 @@ def random_comb(gen: np.random.Generator, comb_size: int, n_tables: int) -> np.n
 
 def random_words(gen: np.random.Generator, shape) -> np.ndarray:
     return gen.integers(0, 2**32, size=shape, dtype=np.uint64).astype(np.uint32)
+
+
+# ---------------------------------------------------- Blum-Goldwasser inputs
+_MR_BASES = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+
+
+def _is_prime(v: int) -> bool:
+    """Deterministic Miller-Rabin for v < 3.3e24 (key generation input only)."""
+    if v < 2:
+        return False
+    for p in _MR_BASES:
+        if v % p == 0:
+            return v == p
+    d, s = v - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in _MR_BASES:
+        x = pow(a, d, v)
+        if x in (1, v - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % v
+            if x == v - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def blum_prime(gen: np.random.Generator, bits: int) -> int:
+    """A random prime p = 3 (mod 4) with the given bit length."""
+    while True:
+        v = int(gen.integers(2 ** (bits - 1), 2**bits)) | 3
+        if _is_prime(v):
+            return v
+
+
+def bg_keys(gen: np.random.Generator, count: int, bits: int):
+    """count key pairs (p, q, N = p q) with p != q Blum primes of `bits` bits."""
+    out = []
+    while len(out) < count:
+        p, q = blum_prime(gen, bits), blum_prime(gen, bits)
+        if p != q:
+            out.append((p, q, p * q))
+    return out
