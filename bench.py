@@ -432,6 +432,17 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: BGm.encrypt(True, Nt, rt, msg, S0), 10)
     res["cbg_encrypt"] = {"value": Bm * Lm / s, "unit": "keystream units/s", "ms_per_call": s * 1e3,
                           "messages": Bm, "units_per_message": Lm, "modulus_bits": 62, "unit_bits": 5}
+    del msg
+    # NEXT-4: Algorithm 1 (single-cell chaotic iterations, f = vectorial
+    # negation on 32 cells, b = 8 -> 10..17 updates per output), 2^20 streams
+    from paper_1112_5239_b200 import chaos as CH
+
+    Sa, na = 2**20, 64
+    za = torch.from_numpy(gen.integers(1, 2**31, Sa).astype(np.int32)).to(dev)
+    xa = torch.zeros(Sa, dtype=torch.int32, device=dev)
+    s = timed(lambda: CH.alg1_generate(32, 8, za, xa, na), 10)
+    res["alg1_negation_b8"] = {"value": Sa * na / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": Sa,
+                               "n": na, "cells": 32, "b": 8}
     return res
 
 

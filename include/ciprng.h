@@ -237,6 +237,36 @@ CIPRNG_API int prng_cbg_decrypt(int chaotic, uint64_t n_msgs, uint64_t L, const 
                                 const uint64_t *y_dev, uint8_t *m_dev, uint32_t *status_dev, void *stream);
 
 /* ---------------------------------------------------------------------- */
+/* Algorithm 1 and the chaos / uniformity checks    */
+/* ---------------------------------------------------------------------- */
+
+/* Algorithm 1 "PRNG with chaotic functions" on n_streams
+ * independent streams, n_out calls each (reading Q34): per call
+ * k = b + XORshift(b), then k + 1 single-cell updates x <- F_f(s, x) with
+ * s = XORshift(n) (cells 1..n = bits 0..n-1; F_f replaces bit s-1 of x by
+ * bit s-1 of f(x), Def. 1); XORshift(m) = 1 + (Alg. 2 xorshift32() mod m)
+ * from the stream's state z, drawn in program order.
+ *   f_dev    NULL = vectorial negation (n <= 32), else 2^n u32 table f(x)
+ *            (n <= 16), entries < 2^n
+ *   z_dev, x_dev [n_streams] u32 xorshift32 states (non-zero) and
+ *            configurations, advanced in place
+ *   out_dev  [n_streams][n_out] u32: the configuration returned by each call
+ * Errors: PRNG_EINVAL (n, b == 0, NULL), PRNG_ESIZE, PRNG_ECUDA. */
+CIPRNG_API int prng_alg1_generate(const uint32_t *f_dev, uint32_t n, uint32_t b, uint32_t *z_dev, uint32_t *x_dev,
+                                  uint64_t n_streams, uint64_t n_out, uint32_t *out_dev, void *stream);
+
+/* Theorems 1 and 2 for f: B^n -> B^n, n <= 16 (f_dev as above,
+ * NULL = negation).  Writes report_dev[3] (u64): [0] vertices of the
+ * iteration graph Gamma(f) reachable from 0, [1] vertices from which 0 is
+ * reachable, [2] vertices whose in- and out-degree (non-loop arcs) differ.
+ * G_f is chaotic (Devaney) iff Gamma(f) is strongly connected iff
+ * [0] == [1] == 2^n; the Markov matrix M of Theorem 2 is doubly stochastic
+ * iff [2] == 0.  scratch_dev: 2^n bytes, caller-owned.  One CTA;
+ * level-synchronous breadth-first search. */
+CIPRNG_API int prng_gamma_check(const uint32_t *f_dev, uint32_t n, uint8_t *scratch_dev, uint64_t *report_dev,
+                                void *stream);
+
+/* ---------------------------------------------------------------------- */
 /* Introspection, checkpoint / test hooks                                 */
 /* ---------------------------------------------------------------------- */
 

@@ -69,6 +69,10 @@ def lib():
         L.orc_cbg_encrypt.restype = i32
         L.orc_cbg_decrypt.argtypes = [i32, u64, u64, u32, u64, vp, u64, vp]
         L.orc_cbg_decrypt.restype = i32
+        L.orc_alg1_generate.argtypes = [vp, u32, u32, vp, vp, u64, u64, vp]
+        L.orc_alg1_generate.restype = i32
+        L.orc_gamma_check.argtypes, L.orc_gamma_check.restype = [vp, u32, vp], i32
+        L.orc_gamma_reach.argtypes, L.orc_gamma_reach.restype = [vp, u32, vp], i32
         _lib = L
     return _lib
 
@@ -214,6 +218,35 @@ def cbg_decrypt(chaotic: bool, p: int, q: int, S0: int, c, y: int) -> np.ndarray
     if lib().orc_cbg_decrypt(int(chaotic), p, q, S0, c.size, _ptr(c), y, _ptr(m)) != 0:
         raise OracleError("cbg_decrypt: invalid key or ciphertext")
     return m
+
+
+# ------------------------------------------------ Algorithm 1 + Gamma(f) (NEXT-4)
+def alg1_generate(f, n: int, b: int, z: np.ndarray, x: np.ndarray, n_out: int) -> np.ndarray:
+    """Algorithm 1, n_out calls per stream; z, x (uint32 [S]) advance in place."""
+    ft = None if f is None else np.ascontiguousarray(f, dtype=np.uint32)
+    S = z.size
+    out = np.zeros((S, n_out), dtype=np.uint32)
+    rc = lib().orc_alg1_generate(_ptr(ft), n, b, _ptr(z), _ptr(x), S, n_out, _ptr(out))
+    if rc != 0:
+        raise OracleError("alg1_generate")
+    return out
+
+
+def gamma_check(f, n: int) -> dict:
+    ft = None if f is None else np.ascontiguousarray(f, dtype=np.uint32)
+    rep = np.zeros(3, np.uint64)
+    if lib().orc_gamma_check(_ptr(ft), n, _ptr(rep)) != 0:
+        raise OracleError("gamma_check")
+    return {"scc": int(rep[0]), "doubly_stochastic": bool(rep[1]), "unbalanced": int(rep[2])}
+
+
+def gamma_reach(f, n: int) -> np.ndarray:
+    """[reachable from 0, reaching 0, unbalanced vertices] (orc_gamma_reach)."""
+    ft = None if f is None else np.ascontiguousarray(f, dtype=np.uint32)
+    rep = np.zeros(3, np.uint64)
+    if lib().orc_gamma_reach(_ptr(ft), n, _ptr(rep)) != 0:
+        raise OracleError("gamma_reach")
+    return rep
 
 
 def digest(words: np.ndarray, first_stream: int = 0) -> int:

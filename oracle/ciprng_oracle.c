@@ -782,6 +782,172 @@ int orc_cbg_decrypt(int chaotic, uint64_t p, uint64_t q, uint32_t S0, uint64_t L
     return ORC_OK;
 }
 
+/* ======================================================================== */
+/* NEXT-4: Algorithm 1 "PRNG with chaotic functions" and the     */
+/* chaos / uniformity checks of Theorems 1-2.                   */
+/* Reading Q34: cells i in [1, n] are bits i-1; F_f(i, x) replaces bit i-1   */
+/* of x by bit i-1 of f(x) (Def. 1); XORshift(m) = 1 + (xorshift32() mod m)  */
+/* from Alg. 2's generator, one state per stream, drawn in      */
+/* program order (first for k, then one per iteration); k = b + XORshift(b)  */
+/* and the loop "for i = 0, ..., k" runs k + 1 iterations.  f = NULL is the  */
+/* vectorial negation; otherwise a table of 2^n entries.        */
+/* ======================================================================== */
+static uint32_t xorshift_range(uint32_t *z, uint32_t m) { return 1u + orc_xorshift32(z) % m; }
+
+static uint32_t apply_single(const uint32_t *f, uint32_t n, uint32_t i, uint32_t x)
+{
+    uint32_t fx = f ? f[x] : (~x & (n == 32 ? 0xFFFFFFFFu : ((1u << n) - 1u)));
+    uint32_t bit = 1u << (i - 1u);
+    return (x & ~bit) | (fx & bit);
+}
+
+/* One call of Algorithm 1 per stream, repeated n_out times: out[s*n_out + j]
+ * is the configuration returned by the j-th call.  z: xorshift32 states,
+ * x: configurations (both advanced in place). */
+int orc_alg1_generate(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *z, uint32_t *x, uint64_t n_streams,
+                      uint64_t n_out, uint32_t *out)
+{
+    uint64_t s, j;
+    uint32_t i, k;
+    if (n == 0 || n > 32 || (f && n > 16) || b == 0) return ORC_EINVAL;
+    for (s = 0; s < n_streams; s++) {
+        for (j = 0; j < n_out; j++) {
+            k = b + xorshift_range(&z[s], b);
+            for (i = 0; i <= k; i++)
+                x[s] = apply_single(f, n, xorshift_range(&z[s], n), x[s]);
+            out[s * n_out + j] = x[s];
+        }
+    }
+    return ORC_OK;
+}
+
+/* Gamma(f): an arc x -> F_f(i, x) for every cell i.  Counts its
+ * strongly connected components (plain iterative Kosaraju over 2^n vertices)
+ * and checks Theorem 2's doubly-stochastic condition: with M_ij = Mc_ij / n
+ * off the diagonal and M_ii = 1 - (1/n) sum_j Mc_ij, the rows sum to 1 by
+ * construction and column j sums to 1 - outdeg(j)/n + indeg(j)/n, so M is
+ * doubly stochastic iff every vertex has equal in- and out-degree counting
+ * non-loop arcs.  report[0] = #SCC, report[1] = 1 if doubly stochastic,
+ * report[2] = #vertices with indeg != outdeg. */
+int orc_gamma_check(const uint32_t *f, uint32_t n, uint64_t *report)
+{
+    uint32_t V, v, i, w, top, cnt = 0;
+    uint32_t *order, *stack, *comp, *indeg, *outdeg, *it, nord = 0;
+    unsigned char *seen;
+    if (n == 0 || n > 16) return ORC_EINVAL;
+    V = 1u << n;
+    order = (uint32_t *)malloc(V * sizeof(uint32_t));
+    stack = (uint32_t *)malloc(V * sizeof(uint32_t));
+    comp = (uint32_t *)malloc(V * sizeof(uint32_t));
+    indeg = (uint32_t *)calloc(V, sizeof(uint32_t));
+    outdeg = (uint32_t *)calloc(V, sizeof(uint32_t));
+    it = (uint32_t *)calloc(V, sizeof(uint32_t));
+    seen = (unsigned char *)calloc(V, 1);
+    for (v = 0; v < V; v++)
+        for (i = 1; i <= n; i++) {
+            w = apply_single(f, n, i, v);
+            if (w != v) { outdeg[v]++; indeg[w]++; }
+        }
+    /* pass 1: DFS finishing order on Gamma(f) */
+    for (v = 0; v < V; v++) {
+        if (seen[v]) continue;
+        top = 0; stack[top++] = v; seen[v] = 1; it[v] = 1;
+        while (top) {
+            uint32_t u = stack[top - 1];
+            if (it[u] <= n) {
+                w = apply_single(f, n, it[u], u);
+                it[u]++;
+                if (!seen[w]) { seen[w] = 1; it[w] = 1; stack[top++] = w; }
+            } else {
+                order[nord++] = u;
+                top--;
+            }
+        }
+    }
+    /* pass 2: DFS on the transpose in reverse finishing order; the transpose
+     * arcs into u are found by scanning the n candidate predecessors u with
+     * bit i-1 flipped or kept (F_f(i, p) differs from p only in bit i-1). */
+    for (v = 0; v < V; v++) comp[v] = 0xFFFFFFFFu;
+    while (nord) {
+        v = order[--nord];
+        if (comp[v] != 0xFFFFFFFFu) continue;
+        top = 0; stack[top++] = v; comp[v] = cnt;
+        while (top) {
+            uint32_t u = stack[--top];
+            for (i = 1; i <= n; i++) {
+                uint32_t cand[2], c;
+                cand[0] = u; cand[1] = u ^ (1u << (i - 1u));
+                for (c = 0; c < 2; c++) {
+                    uint32_t pz = cand[c];
+                    if (apply_single(f, n, i, pz) == u && comp[pz] == 0xFFFFFFFFu) {
+                        comp[pz] = cnt;
+                        stack[top++] = pz;
+                    }
+                }
+            }
+        }
+        cnt++;
+    }
+    report[0] = cnt;
+    report[2] = 0;
+    for (v = 0; v < V; v++) report[2] += (indeg[v] != outdeg[v]);
+    report[1] = report[2] == 0;
+    free(order); free(stack); free(comp); free(indeg); free(outdeg); free(it); free(seen);
+    return ORC_OK;
+}
+
+/* Reachability form of Theorem 1's test, used for GPU parity: report[0] =
+ * vertices reachable from vertex 0 in Gamma(f), report[1] = vertices from
+ * which vertex 0 is reachable, report[2] = vertices with in-degree !=
+ * out-degree (non-loop arcs).  Gamma(f) is strongly connected iff
+ * report[0] == report[1] == 2^n; Theorem 2's M is doubly stochastic iff
+ * report[2] == 0.  Plain breadth-first search with a queue. */
+int orc_gamma_reach(const uint32_t *f, uint32_t n, uint64_t *report)
+{
+    uint32_t V, v, i, head, tail, dir;
+    uint32_t *queue, *indeg, *outdeg;
+    unsigned char *seen;
+    if (n == 0 || n > 16) return ORC_EINVAL;
+    V = 1u << n;
+    queue = (uint32_t *)malloc(V * sizeof(uint32_t));
+    indeg = (uint32_t *)calloc(V, sizeof(uint32_t));
+    outdeg = (uint32_t *)calloc(V, sizeof(uint32_t));
+    seen = (unsigned char *)malloc(V);
+    for (dir = 0; dir < 2; dir++) {
+        memset(seen, 0, V);
+        head = tail = 0;
+        queue[tail++] = 0;
+        seen[0] = 1;
+        while (head < tail) {
+            uint32_t u = queue[head++];
+            for (i = 1; i <= n; i++) {
+                if (dir == 0) { /* arcs u -> F_f(i, u) */
+                    uint32_t w = apply_single(f, n, i, u);
+                    if (!seen[w]) { seen[w] = 1; queue[tail++] = w; }
+                } else {        /* arcs p -> u: p in {u, u ^ bit(i-1)} with F_f(i, p) == u */
+                    uint32_t cand[2], c;
+                    cand[0] = u; cand[1] = u ^ (1u << (i - 1u));
+                    for (c = 0; c < 2; c++)
+                        if (apply_single(f, n, i, cand[c]) == u && !seen[cand[c]]) {
+                            seen[cand[c]] = 1;
+                            queue[tail++] = cand[c];
+                        }
+                }
+            }
+        }
+        report[dir] = tail;
+    }
+    for (v = 0; v < V; v++)
+        for (i = 1; i <= n; i++) {
+            uint32_t w = apply_single(f, n, i, v);
+            if (w != v) { outdeg[v]++; indeg[w]++; }
+        }
+    report[2] = 0;
+    for (v = 0; v < V; v++) report[2] += (indeg[v] != outdeg[v]);
+    free(queue); free(indeg); free(outdeg); free(seen);
+    return ORC_OK;
+}
+
 /* Verification digest (reading Q28): sum over the call's words of
  * mix64(mix64(idx) ^ x_idx) mod 2^64, idx = (first_stream + s) * n + i. */
 uint64_t orc_digest_words(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n)

@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
             "prng_battery": ([vp, u64, vp, vp], i32),
             "prng_cbg_encrypt": ([i32, u64, u64, vp, vp, vp, vp, vp, vp, vp], i32),
             "prng_cbg_decrypt": ([i32, u64, u64, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+            "prng_alg1_generate": ([vp, u32, u32, vp, vp, u64, u64, vp, vp], i32),
+            "prng_gamma_check": ([vp, u32, vp, vp, vp], i32),
             "prng_digest": ([vp, u64, u64, u64, vp, vp], i32),
             "prng_get_info": ([vp, ctypes.POINTER(PrngInfo)], i32),
             "prng_get_state": ([vp, vp, sz], i32),

@@ -555,6 +555,24 @@ int prng_cbg_decrypt(int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *p
     return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
 }
 
+int prng_alg1_generate(const uint32_t *f_dev, uint32_t n, uint32_t b, uint32_t *z_dev, uint32_t *x_dev,
+                       uint64_t n_streams, uint64_t n_out, uint32_t *out_dev, void *stream) {
+    if (n == 0 || n > 32 || (f_dev && n > 16) || b == 0) return PRNG_EINVAL;
+    if (n_streams == 0 || n_out == 0) return PRNG_OK;
+    if (!z_dev || !x_dev || !out_dev) return PRNG_EINVAL;
+    if (n_streams > SIZE_MAX / 4 / n_out) return PRNG_ESIZE;
+    launch_alg1(f_dev, n, b, z_dev, x_dev, n_streams, n_out, out_dev, (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
+}
+
+int prng_gamma_check(const uint32_t *f_dev, uint32_t n, uint8_t *scratch_dev, uint64_t *report_dev, void *stream) {
+    if (n == 0 || n > 16 || !scratch_dev || !report_dev) return PRNG_EINVAL;
+    launch_gamma(f_dev, n, scratch_dev, reinterpret_cast<unsigned long long *>(report_dev), (cudaStream_t)stream);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PRNG_OK : cuda_fail(e);
+}
+
 int prng_get_info(const prng_t *h, prng_info_t *info) {
     if (!h || !info) return PRNG_EINVAL;
     info->variant = h->variant;

@@ -127,6 +127,11 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ uint64_t l2_evict_normal_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 // State-plane accesses with an L2 policy (evict-last keeps the planes, read
 // and rewritten every call, resident while the output streams through L2).
 __device__ __forceinline__ uint32_t ld_state(const uint32_t *p, uint64_t pol) {
@@ -206,24 +211,19 @@ struct GenArgs {
     CombTables comb;
 };
 
-// SoA state-plane access (plane k of local stream s at word k*L + s) with the
-// evict-last L2 hint when enabled (a.state_last).
+// SoA state-plane access (plane k of local stream s at word k*L + s).  Every
+// access carries an L2 cache-policy operand chosen once per kernel --
+// evict-last when a.state_last, else evict-normal -- so there is no
+// per-access branch (a branch per load serialised V2's dependent modulus
+// loads: -10 %, gpurun_out/s14).
 struct StateIO {
     uint32_t *P;
     uint64_t L;
     uint64_t pol;
-    bool last;
     __device__ __forceinline__ explicit StateIO(const GenArgs &a)
-        : P(a.state), L(a.n_local), pol(l2_evict_last_policy()), last(a.state_last != 0) {}
-    __device__ __forceinline__ uint32_t ld(uint32_t k, uint64_t s) const {
-        const uint32_t *p = P + k * L + s;
-        return last ? ld_state(p, pol) : *p;
-    }
-    __device__ __forceinline__ void st(uint32_t k, uint64_t s, uint32_t v) const {
-        uint32_t *p = P + k * L + s;
-        if (last) st_state(p, v, pol);
-        else *p = v;
-    }
+        : P(a.state), L(a.n_local), pol(a.state_last ? l2_evict_last_policy() : l2_evict_normal_policy()) {}
+    __device__ __forceinline__ uint32_t ld(uint32_t k, uint64_t s) const { return ld_state(P + k * L + s, pol); }
+    __device__ __forceinline__ void st(uint32_t k, uint64_t s, uint32_t v) const { st_state(P + k * L + s, v, pol); }
 };
 
 }  // namespace ciprng

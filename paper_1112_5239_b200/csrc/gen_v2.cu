@@ -83,18 +83,26 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         const bool valid = row < a.s_count;
         const uint64_t s = a.s_begin + row;
         Bbs8 b;
-        uint32_t x = 0, tp = 0;
+        // every lane loads (an invalid lane reads the tile's first row and
+        // discards it): no branch between the 8 dependent state -> modulus loads
+        const uint64_t sl = valid ? s : a.s_begin + tile * 32;
+        uint32_t m[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            b.y[j] = valid ? sio.ld(j, s) : 2u;
-            const uint32_t m = valid ? sio.ld(8 + j, s) : 0u;
-            const uint4 e = __ldg(modtab + m);  // {M, mu, 2^32 - M, 0}
+            b.y[j] = sio.ld(j, sl);
+            m[j] = sio.ld(8 + j, sl);
+        }
+        uint32_t x = sio.ld(16, sl), tp = sio.ld(17, sl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 e = __ldg(modtab + m[j]);  // {M, mu, 2^32 - M, 0}
             b.mu[j] = e.y;
             b.nM[j] = e.z;
         }
-        if (valid) {
-            x = sio.ld(16, s);
-            tp = sio.ld(17, s);
+        if (!valid) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b.y[j] = 2u;
+            x = tp = 0;
         }
         const uint32_t src1 = gbase + a.comb.t[b.y[0] & 7u][off];
         const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
@@ -115,9 +123,8 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         sink.end_rows(valid ? 1u : 0u);
         if (valid && a.n > 0) {
             // rotation (Q19): instance j moves to slot j+1 with its modulus
-            // index, which is re-read from the untouched call-entry plane
-            // instead of being held in 8 registers through the loop
-            uint32_t m[8];
+            // index, re-read from the untouched call-entry plane instead of
+            // being held in 8 registers through the loop
 #pragma unroll
             for (int j = 0; j < 8; ++j) m[j] = sio.ld(8 + j, s);
 #pragma unroll

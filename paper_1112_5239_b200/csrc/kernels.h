@@ -88,6 +88,9 @@ int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
 int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
 int launch_cbg(bool encrypt, int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *a0, const uint64_t *a1,
                const uint32_t *S0, const uint8_t *in, uint8_t *out, uint64_t *y, uint32_t *status, cudaStream_t st);
+int launch_alg1(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *z, uint32_t *x, uint64_t n_streams,
+                uint64_t n_out, uint32_t *out, cudaStream_t st);
+int launch_gamma(const uint32_t *f, uint32_t n, uint8_t *mark, unsigned long long *report, cudaStream_t st);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);
 

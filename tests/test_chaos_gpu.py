@@ -1,0 +1,59 @@
+"""GPU Algorithm 1 and Gamma(f) checks against the
+oracle: bit-exact configurations for negation and table functions, in-place
+state advance, and identical reachability / balance reports."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import workloads as W
+from paper_1112_5239_b200 import chaos as C
+
+pytestmark = pytest.mark.gpu
+
+
+def _i32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+
+
+@pytest.mark.parametrize("n,b,table", [(4, 1, False), (16, 8, False), (32, 3, False), (4, 5, True), (12, 8, True),
+                                       (16, 2, True)])
+def test_alg1_matches_oracle(n, b, table):
+    gen = W.rng(700 + n + b)
+    S, n_out = 1000, 37
+    f = gen.integers(0, 2**n, 2**n).astype(np.uint32) if table else None
+    z = gen.integers(1, 2**32, S).astype(np.uint32)
+    x = (gen.integers(0, 2**32, S) & ((1 << n) - 1 if n < 32 else 0xFFFFFFFF)).astype(np.uint32)
+    zt, xt = _i32(z), _i32(x)
+    got = C.alg1_generate(n, b, zt, xt, n_out, f=None if f is None else _i32(f))
+    zr, xr = z.copy(), x.copy()
+    ref = O.alg1_generate(f, n, b, zr, xr, n_out)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), ref)
+    assert np.array_equal(zt.cpu().numpy().view(np.uint32), zr)
+    assert np.array_equal(xt.cpu().numpy().view(np.uint32), xr)
+
+
+@pytest.mark.parametrize("case", ["negation", "identity", "constant", "random", "perturbed", "perm"])
+@pytest.mark.parametrize("n", [2, 6, 11, 16])
+def test_gamma_check_matches_oracle(case, n):
+    gen = W.rng(800 + n)
+    V = 2**n
+    if case == "negation":
+        f = None
+    elif case == "identity":
+        f = np.arange(V, dtype=np.uint32)
+    elif case == "constant":
+        f = np.zeros(V, np.uint32)
+    elif case == "random":
+        f = gen.integers(0, V, V).astype(np.uint32)
+    elif case == "perturbed":
+        f = (~np.arange(V, dtype=np.uint32)) & (V - 1)
+        f[gen.integers(0, V, 3)] ^= 1
+        f = f.astype(np.uint32)
+    else:
+        f = gen.permutation(V).astype(np.uint32)
+    got = C.gamma_check(n, None if f is None else _i32(f))
+    ref = O.gamma_reach(f, n)
+    assert [got["reach_from_0"], got["reach_to_0"], got["unbalanced"]] == ref.tolist()
+    if case == "negation":
+        assert got["chaotic"] and got["doubly_stochastic"]
