@@ -64,6 +64,35 @@ def ncu_traffic():
     return None
 
 
+# Integer-issue peak for the compute-bound rows: one warp
+# instruction per scheduler per clock = 148 SMs x 4 x 32 lanes x 1.965 GHz.
+ISSUE_PEAK_TLANE = 148 * 4 * 32 * 1.965e9 / 1e12
+# ncu capture kind (tools/prof_kernels.py) -> (secondary key, numbers per launch)
+NCU_KINDS = {"v2": ("c3_v2_store", 2**20 * 64), "v0": ("v0_store", 2**20 * 128), "v3": ("v3_store", 2**20 * 128),
+             "v4": ("v4_store", 2**20 * 128), "consume": ("c5_v1_consume", 2**20 * 1024)}
+
+
+def ncu_inst_per_number():
+    """lane instructions per number of each secondary kernel, from the newest
+    committed ncu capture (profiles/r*_ncu_summary.json: smsp__inst_executed x
+    32 lanes / numbers in the profiled launch)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        with open(f) as fh:
+            caps = json.load(fh).get("captures", {})
+        out = {}
+        for kind, (key, numbers) in NCU_KINDS.items():
+            for c in caps.get(kind, []):
+                if c.get("warp_insts"):
+                    out[key] = (c["warp_insts"] * 32 / numbers, os.path.relpath(f, ROOT), c.get("kernel"))
+                    break
+        if out:
+            return out
+    return {}
+
+
 class ClockSampler:
     """NVML clock / throttle-reason sampling during the timed region."""
 
@@ -287,6 +316,14 @@ def run_ours(args):
     secondary = {}
     if not args.no_secondary:
         secondary = measure_secondary(P, torch, dev, args)
+        for key, (ipn, src, kern) in ncu_inst_per_number().items():
+            if key in secondary:
+                ach = secondary[key]["value"] * ipn / 1e12
+                secondary[key]["roofline"] = {
+                    "bound": "alu", "achieved": ach, "peak": ISSUE_PEAK_TLANE, "unit": "T lane-inst/s",
+                    "frac": ach / ISSUE_PEAK_TLANE, "inst_per_number": ipn, "kernel": kern,
+                    "source": f"{src} (smsp__inst_executed x 32 / numbers); peak = 148 SMs x 4 schedulers x 32 "
+                              "lanes x 1.965 GHz (DESIGN.md s6)"}
 
     line = {
         "metric": METRIC,
