@@ -1,6 +1,9 @@
 // api.cu -- the C ABI of include/ciprng.h: argument checking, device state
 // ownership, kernel-path selection and the pipelined device->host path.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -92,6 +95,22 @@ constexpr int kStateWords[5] = {23, 6, 18, 4, 24};
 }  // namespace
 
 thread_local ciprng::L2Window ciprng::g_l2win;
+
+int ciprng::resident_blocks(const void *kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, size_t, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(kern, threads, smem, dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) per = 1;
+    cudaGetLastError();
+    return cache[key] = per * sms;
+}
 
 static bool env_on(const char *name, bool dflt) {
     const char *v = std::getenv(name);
@@ -344,6 +363,10 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
     if (const char *v = std::getenv("CIPRNG_V1_WPB")) {
         int w = std::atoi(v);
         if (w >= 1 && w <= 8) h->v1tune.wpb = w;
+    }
+    if (const char *v = std::getenv("CIPRNG_V1_TPW")) {
+        int t = std::atoi(v);
+        if (t >= 1 && t <= 64) h->v1tune.tiles_per_warp = t;
     }
     if (const char *v = std::getenv("CIPRNG_V1_GRID")) {
         int b = std::atoi(v);

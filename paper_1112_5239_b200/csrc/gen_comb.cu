@@ -241,21 +241,25 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
         } else if (mode == 0) {
             launch_k(comb_fast_kernel<Src, StoreSink, 0>, dim3(comb_blocks(tiles, 4, 0)), dim3(128), 0, st, a, *tmap);
         } else if (mode == 2) {
-            launch_k(comb_fast_kernel<Src, StatsSink, 0>, dim3(comb_blocks(tiles, 4, persistent_blocks)), dim3(128),
-                     4 * StatsSink::kSmemBytesPerWarp, st, a, *tmap);
+            auto kern = comb_fast_kernel<Src, StatsSink, 0>;
+            const size_t sm = 4 * StatsSink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);
         } else {
-            launch_k(comb_fast_kernel<Src, BatterySink, 0>, dim3(comb_blocks(tiles, 4, persistent_blocks)), dim3(128),
-                     4 * BatterySink::kSmemBytesPerWarp, st, a, *tmap);
+            auto kern = comb_fast_kernel<Src, BatterySink, 0>;
+            const size_t sm = 4 * BatterySink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;
         const int wpb = 8;
         if (mode == 2) {
-            launch_k(comb_general_kernel<Src, StatsSink>, dim3(comb_blocks(tiles, wpb, persistent_blocks)),
-                     dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+            auto kern = comb_general_kernel<Src, StatsSink>;
+            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, (tiles + wpb - 1) / wpb)), dim3(32 * wpb), sm, st, a);
         } else if (mode == 3) {
-            launch_k(comb_general_kernel<Src, BatterySink>, dim3(comb_blocks(tiles, wpb, persistent_blocks)),
-                     dim3(32 * wpb), wpb * BatterySink::kSmemBytesPerWarp, st, a);
+            auto kern = comb_general_kernel<Src, BatterySink>;
+            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, (tiles + wpb - 1) / wpb)), dim3(32 * wpb), sm, st, a);
         } else {
             launch_k(comb_general_kernel<Src, StoreSink>, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), 0, st, a);
         }

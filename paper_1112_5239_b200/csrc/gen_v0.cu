@@ -139,14 +139,15 @@ static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st, int persisten
     const uint64_t tiles = (a.s_count + 31) / 32;
     const int wpb = 8;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
+    (void)persistent_blocks;
     if (mode == 2) {
-        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
-        launch_k(v0_kernel<StatsSink, kComb>, dim3((int)blocks), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp,
-                 st, a);
+        auto kern = v0_kernel<StatsSink, kComb>;
+        const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+        launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else if (mode == 3) {
-        if (persistent_blocks > 0 && blocks > (uint64_t)persistent_blocks) blocks = persistent_blocks;
-        launch_k(v0_kernel<BatterySink, kComb>, dim3((int)blocks), dim3(32 * wpb),
-                 wpb * BatterySink::kSmemBytesPerWarp, st, a);
+        auto kern = v0_kernel<BatterySink, kComb>;
+        const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+        launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else {
         launch_k(v0_kernel<StoreSink, kComb>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }

@@ -94,7 +94,7 @@ constexpr int kFastTileRows = 64;
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
 // TMA tile store of kCols rounds x 64 streams per box, double-buffered.
 template <class Sink, int kCols>
-__global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(256, 4) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);
@@ -401,7 +401,9 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
     if (fast) {
         const uint64_t tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
         const int wpb = tune.wpb > 0 ? tune.wpb : 4;
-        const int cap = tune.grid_blocks > 0 ? tune.grid_blocks : 0;
+        int cap = tune.grid_blocks > 0 ? tune.grid_blocks : 0;
+        if (cap == 0 && tune.tiles_per_warp > 1)
+            cap = (int)((tiles + (uint64_t)wpb * tune.tiles_per_warp - 1) / ((uint64_t)wpb * tune.tiles_per_warp));
         CUtensorMap dummy;
         if (tmap == nullptr) tmap = &dummy;
         if (mode == 0) {
@@ -414,24 +416,29 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             else if (tune.cols == 32) launch_fast_tma<32>(a, *tmap, grid, wpb, st);
             else launch_fast_tma<16>(a, *tmap, grid, wpb, st);
         } else {
-            int grid = blocks_for(tiles, 4, persistent_blocks);
-            if (mode == 3)
-                launch_k(v1_fast_kernel<BatterySink, 0>, dim3(grid), dim3(128), 4 * BatterySink::kSmemBytesPerWarp, st,
-                         a, *tmap);
-            else
-                launch_k(v1_fast_kernel<StatsSink, 0>, dim3(grid), dim3(128), 4 * StatsSink::kSmemBytesPerWarp, st, a,
-                         *tmap);
+            const uint64_t need = (tiles + 3) / 4;
+            if (mode == 3) {
+                auto kern = v1_fast_kernel<BatterySink, 0>;
+                const size_t sm = 4 * BatterySink::kSmemBytesPerWarp;
+                launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
+            } else {
+                auto kern = v1_fast_kernel<StatsSink, 0>;
+                const size_t sm = 4 * StatsSink::kSmemBytesPerWarp;
+                launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
+            }
         }
     } else {
         const uint64_t tiles = (a.s_count + 31) / 32;
         const int wpb = 8;
+        const uint64_t need = (tiles + wpb - 1) / wpb;
         if (mode == 2) {
-            int grid = blocks_for(tiles, wpb, persistent_blocks);
-            launch_k(v1_general_kernel<StatsSink>, dim3(grid), dim3(32 * wpb), wpb * StatsSink::kSmemBytesPerWarp, st, a);
+            auto kern = v1_general_kernel<StatsSink>;
+            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, need)), dim3(32 * wpb), sm, st, a);
         } else if (mode == 3) {
-            int grid = blocks_for(tiles, wpb, persistent_blocks);
-            launch_k(v1_general_kernel<BatterySink>, dim3(grid), dim3(32 * wpb), wpb * BatterySink::kSmemBytesPerWarp,
-                     st, a);
+            auto kern = v1_general_kernel<BatterySink>;
+            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+            launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, need)), dim3(32 * wpb), sm, st, a);
         } else {
             int grid = blocks_for(tiles, wpb, 0);
             launch_k(v1_general_kernel<StoreSink>, dim3(grid), dim3(32 * wpb), 0, st, a);

@@ -55,6 +55,18 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Blocks of `kern` that are resident at once on the device (occupancy x SMs):
+// the grid of the persistent consumer / battery kernels.  A fixed 8 CTAs/SM
+// overshoots when registers limit residency to 7 (the consumer), leaving a
+// second partial wave.
+int resident_blocks(const void *kern, int threads, size_t smem);
+template <typename... KArgs>
+inline int persistent_grid(void (*kern)(KArgs...), int threads, size_t smem, uint64_t blocks_needed) {
+    const int r = resident_blocks(reinterpret_cast<const void *>(kern), threads, smem);
+    const uint64_t b = blocks_needed < (uint64_t)r ? blocks_needed : (uint64_t)r;
+    return (int)(b ? b : 1);
+}
+
 struct InitArgs {
     uint32_t *state;
     uint64_t n_local;
@@ -73,6 +85,7 @@ struct V1Tuning {
                           // 64, 128 (3-D band boxes, needs n % 32 == 0)
     int wpb = 2;          // warps per CTA
     int grid_blocks = 0;  // 2-D kernels: 0 = one 64-stream tile per warp, > 0 = grid cap
+    int tiles_per_warp = 1;  // 2-D kernels without a cap: grid = tiles / (wpb * tiles_per_warp)
     int grid_mode = 0;    // band kernels: 0 = one tile per warp, -1 = persistent at
                           // full occupancy, k > 0 = persistent with k CTAs per SM
 };

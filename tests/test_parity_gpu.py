@@ -333,3 +333,12 @@ def test_battery_1e10_numbers(variant):
         g.battery(n, stats)
     p = B.pvalues(P.as_u64(stats), S * calls, n)
     assert B.passes(p, alpha=1e-4), p
+
+
+@pytest.mark.parametrize("tpw", [2, 3])
+def test_v1_store_tiles_per_warp(monkeypatch, tpw):
+    """Several 64-stream tiles per warp (state of the next tile prefetched
+    while the current one computes) stay bit-exact, incl. a ragged last tile."""
+    monkeypatch.setenv("CIPRNG_V1_TPW", str(tpw))
+    for S in (96, 4096 + 32):
+        _check(W.V1, SEEDS[1], S, [4, 36, 128, 20], store_path=P.STORE_TMA)

@@ -1,5 +1,5 @@
 """Small driver for ncu captures: a few calls of one workload through the
-C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|v3|v4|consume} [calls]"""
+C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|v3|v4|consume|battery|cbg|alg1} [calls]"""
 import os
 import sys
 
@@ -36,6 +36,28 @@ elif which in ("v3", "v4"):
     out = torch.empty((S, n), dtype=torch.int32, device="cuda")
     for _ in range(calls):
         g.generate(n, out=out)
+elif which == "battery":
+    S, n = 2**20, 1024
+    g = P.ChaoticPRNG(seed, S, P.V1)
+    st = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    for _ in range(calls):
+        g.battery(n, st)
+elif which == "cbg":
+    from paper_1112_5239_b200 import bg as BG
+
+    Bm, L = 2**18, 1024
+    N = torch.full((Bm,), 3037000493 * 3037000453 % (2**62), dtype=torch.int64, device="cuda") | 1
+    r = torch.randint(2, 2**30, (Bm,), dtype=torch.int64, device="cuda")
+    m = torch.randint(0, 256, (Bm, L), dtype=torch.uint8, device="cuda")
+    for _ in range(calls):
+        BG.encrypt(True, N, r, m)
+elif which == "alg1":
+    from paper_1112_5239_b200 import chaos as CH
+
+    z = torch.randint(1, 2**31, (2**20,), dtype=torch.int32, device="cuda")
+    x = torch.zeros(2**20, dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        CH.alg1_generate(32, 8, z, x, 64)
 elif which == "consume":
     S, n = 2**20, 1024
     g = P.ChaoticPRNG(seed, S, P.V1)
