@@ -150,6 +150,10 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap *map, uint32
         "r"(smem_addr), "r"(c0), "r"(c1), "l"(pol)
         : "memory");
 }
+// L2 prefetch of `bytes` (multiple of 16, 16-byte aligned) global bytes
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -208,6 +212,7 @@ struct GenArgs {
     uint32_t vec;        // 1: rows are 16-byte aligned, n % 4 == 0
     uint32_t evict_first; // 1: output stores carry an L2 evict-first hint
     uint32_t state_last;  // 1: state-plane loads/stores carry an L2 evict-last hint
+    uint32_t pf_ahead;    // V1 TMA store: prefetch into L2 the state of tile + pf_ahead (0 = off)
     CombTables comb;
 };
 

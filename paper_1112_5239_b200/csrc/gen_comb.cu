@@ -233,7 +233,7 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
     if (fast) {
         const uint64_t tiles = (a.s_count + kCombTileRows - 1) / kCombTileRows;
         if (mode == 1) {
-            constexpr int kCols = 32, wpb = 2;
+            constexpr int kCols = 32, wpb = 2;  // V3: wpb 4 measured 1.5 % slower (profiles/experiments/s18)
             const size_t smem = (size_t)wpb * 2 * kCombTileRows * kCols * 4 + 1024;
             auto kern = comb_fast_kernel<Src, StoreSink, kCols>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

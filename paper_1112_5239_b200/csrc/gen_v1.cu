@@ -94,7 +94,7 @@ constexpr int kFastTileRows = 64;
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
 // TMA tile store of kCols rounds x 64 streams per box, double-buffered.
 template <class Sink, int kCols>
-__global__ void __launch_bounds__(256, 4) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);
@@ -140,6 +140,15 @@ __global__ void __launch_bounds__(256, 4) v1_fast_kernel(GenArgs a, const __grid
         const bool valid = row0 + 32u * h < a.s_count;  // s_count % 32 == 0
         const uint64_t rA = row0 + rA_t, rB = row0 + rB_t;
         const uint64_t sA = a.s_begin + rA, sB = a.s_begin + rB;
+        // warm L2 with the state of the tile a warp of the next wave will take
+        // (one wave = pf_ahead resident warps), so its first loads hit L2
+        if (a.pf_ahead && lane == 0) {
+            const uint64_t t2 = tile + a.pf_ahead;
+            if (t2 * kFastTileRows + kFastTileRows <= a.s_count)
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    bulk_prefetch_l2(P + k * L + a.s_begin + t2 * kFastTileRows, kFastTileRows * 4);
+        }
         uint32_t a0 = pa[0], a1 = pa[1], a2 = pa[2], a3 = pa[3], xA = pa[4], tpA = pa[5];
         uint32_t b0 = pb[0], b1 = pb[1], b2 = pb[2], b3 = pb[3], xB = pb[4], tpB = pb[5];
         prefetch(tile + warps);
@@ -386,12 +395,17 @@ static void launch_band(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles,
 }
 
 template <int kCols>
-static void launch_fast_tma(const GenArgs &a, const CUtensorMap &tm, int grid, int wpb, cudaStream_t st) {
+static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, int wpb, bool pf, cudaStream_t st) {
     const size_t smem = (size_t)wpb * 2 * kFastTileRows * kCols * 4 + 1024;  // + alignment slack
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(v1_fast_kernel<StoreSink, kCols>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    launch_k(v1_fast_kernel<StoreSink, kCols>, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
+    auto kern = v1_fast_kernel<StoreSink, kCols>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    GenArgs a = a0;
+    // one wave of resident warps ahead (non-persistent grid: the tile the
+    // warp replacing this one in a later wave will take)
+    a.pf_ahead = pf && grid > resident_blocks(reinterpret_cast<const void *>(kern), 32 * wpb, smem)
+                     ? (uint32_t)(resident_blocks(reinterpret_cast<const void *>(kern), 32 * wpb, smem) * wpb)
+                     : 0u;
+    launch_k(kern, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
@@ -412,9 +426,9 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             const int grid = blocks_for(tiles, wpb, cap);
             if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
             else if (tune.cols == 128) launch_band<4, 1>(a, *tmap, tiles, wpb, tune.grid_mode, st);
-            else if (tune.cols == 8) launch_fast_tma<8>(a, *tmap, grid, wpb, st);
-            else if (tune.cols == 32) launch_fast_tma<32>(a, *tmap, grid, wpb, st);
-            else launch_fast_tma<16>(a, *tmap, grid, wpb, st);
+            else if (tune.cols == 8) launch_fast_tma<8>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
+            else if (tune.cols == 32) launch_fast_tma<32>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
+            else launch_fast_tma<16>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
         } else {
             const uint64_t need = (tiles + 3) / 4;
             if (mode == 3) {

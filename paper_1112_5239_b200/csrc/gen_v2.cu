@@ -27,6 +27,16 @@ struct Bbs8 {
     uint32_t y[8], nM[8], mu[8];  // nM = 2^32 - M
 };
 
+// y << k on the ALU pipe (funnel shift with a zero low word): the heavy FMA
+// sub-pipe is V2's bound (Barrett's IMAD / IMAD.HI), so the nibble
+// placement must not land there as IMAD.SHL.
+template <int k>
+__device__ __forceinline__ uint32_t shl_alu(uint32_t y) {
+    uint32_t r;
+    asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(y), "n"(k));
+    return r;
+}
+
 // bmsk: the low `n` bits set (n in 0..3 here), one BMSK instruction
 __device__ __forceinline__ uint32_t low_mask(uint32_t n) {
     uint32_t m;
@@ -43,8 +53,9 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t n) {
 __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
-    const uint32_t f0 = b.y[0] << 28, f1 = b.y[1] << 24, f2 = b.y[2] << 20, f3 = b.y[3] << 16;
-    const uint32_t f4 = b.y[4] << 12, f5 = b.y[5] << 8, f6 = b.y[6] << 4, f7 = b.y[7];
+    const uint32_t f0 = shl_alu<28>(b.y[0]), f1 = shl_alu<24>(b.y[1]), f2 = shl_alu<20>(b.y[2]);
+    const uint32_t f3 = shl_alu<16>(b.y[3]), f4 = shl_alu<12>(b.y[4]), f5 = shl_alu<8>(b.y[5]);
+    const uint32_t f6 = shl_alu<4>(b.y[6]), f7 = b.y[7];
     const uint32_t p01 = (f0 & 0xF0000000u) | (f1 & ~0xF0000000u);
     const uint32_t p23 = (f2 & 0xFFF00000u) | (f3 & ~0xFFF00000u);
     const uint32_t p45 = (f4 & 0xFFFFF000u) | (f5 & ~0xFFFFF000u);
