@@ -235,42 +235,56 @@ struct StateIO {
 
 namespace ciprng {
 // ------------------------------------------ 64-bit xor-like on 32-bit halves
-// Listing 1's generators on (lo, hi) register pairs, written so that each
-// 64-bit constant shift is one funnel shift (ALU pipe) plus one plain 32-bit
-// shift expressed as a multiply (IMAD.SHL / IMAD.HI: FMA pipe).  Same values
-// as the uint64_t forms above; this only balances the two integer pipes.
-// Measured (ncu r1d): IMAD.HI occupies the heavy FMA sub-pipe twice as long
-// as IMAD.SHL or an ALU op, so writing the funnel halves as multiplies too
-// (IMAD.SHL + IMAD.HI, merged by XOR) made V0 heavy-pipe bound and 15 %
-// slower; this split is the measured optimum.
+// Listing 1's generators on (lo, hi) register pairs.  A 64-bit constant
+// shift has a plain half (one 32-bit shift, written as a multiply: IMAD.SHL
+// or IMAD.HI on the FMA pipe) and a funnel half that combines both words.
+// The funnel half is either one SHF (ALU pipe) or -- template flag kF --
+// two multiplies (IMAD.SHL + IMAD.HI) whose disjoint bit ranges are merged by
+// the XOR that consumes the shift anyway (a 3-input LOP3), moving one ALU op
+// to 6 heavy-FMA cycles.  Measured (ncu r1d/r1h): IMAD.HI holds the heavy
+// sub-pipe twice as long as IMAD.SHL or an ALU op; all-SHF funnels leave V0
+// ALU-bound (86 %) with the FMA pipe at 15 %, all-multiply funnels made V0
+// heavy-bound and 15 % slower, so each generator converts only some shifts.
 struct u64p {
     uint32_t lo, hi;
 };
-__device__ __forceinline__ uint32_t shl32_fma(uint32_t v, int k) { return v * (1u << k); }
-__device__ __forceinline__ uint32_t shr32_fma(uint32_t v, int k) { return __umulhi(v, 1u << (32 - k)); }
-__device__ __forceinline__ u64p shl64(u64p a, int k) {  // a << k, 0 < k < 32
-    return {shl32_fma(a.lo, k), __funnelshift_l(a.lo, a.hi, k)};
+template <int k>
+__device__ __forceinline__ uint32_t mul_pow2(uint32_t v) {  // v << k as IMAD.SHL
+    uint32_t r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(v), "n"(1u << k));
+    return r;
 }
-__device__ __forceinline__ u64p shr64(u64p a, int k) {  // a >> k, 0 < k < 32
-    return {__funnelshift_r(a.lo, a.hi, k), shr32_fma(a.hi, k)};
+template <int k, bool kF = false>
+__device__ __forceinline__ u64p shl64(u64p a) {  // a << k, 0 < k < 32
+    if constexpr (kF) return {mul_pow2<k>(a.lo), mul_pow2<k>(a.hi) ^ shr_fma<32 - k>(a.lo)};
+    else return {mul_pow2<k>(a.lo), __funnelshift_l(a.lo, a.hi, k)};
+}
+template <int k, bool kF = false>
+__device__ __forceinline__ u64p shr64(u64p a) {  // a >> k, 0 < k < 32
+    if constexpr (kF) return {shr_fma<k>(a.lo) ^ mul_pow2<32 - k>(a.hi), shr_fma<k>(a.hi)};
+    else return {__funnelshift_r(a.lo, a.hi, k), shr_fma<k>(a.hi)};
 }
 __device__ __forceinline__ u64p xor64p(u64p a, u64p b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
 __device__ __forceinline__ u64p xor64p(u64p a, u64p b, u64p c) { return {a.lo ^ b.lo ^ c.lo, a.hi ^ b.hi ^ c.hi}; }
+// kF bits select which of a generator's three shifts use the multiply funnel
+template <int kF = 0>
 __device__ __forceinline__ u64p xor64_step_p(u64p a) {
-    a = xor64p(a, shl64(a, 13));
-    a = xor64p(a, shr64(a, 7));
-    a = xor64p(a, shl64(a, 17));
+    a = xor64p(a, shl64<13, (kF & 1) != 0>(a));
+    a = xor64p(a, shr64<7, (kF & 2) != 0>(a));
+    a = xor64p(a, shl64<17, (kF & 4) != 0>(a));
     return a;
 }
+template <int kF = 0>
 __device__ __forceinline__ u64p xor128_f64p(u64p xk, u64p wk3) {
-    u64p t = xor64p(xk, shl64(xk, 11));
-    u64p r = xor64p(wk3, shr64(wk3, 19), t);
-    return xor64p(r, shr64(t, 8));
+    u64p t = xor64p(xk, shl64<11, (kF & 1) != 0>(xk));
+    u64p r = xor64p(wk3, shr64<19, (kF & 2) != 0>(wk3), t);
+    return xor64p(r, shr64<8, (kF & 4) != 0>(t));
 }
+template <int kF = 0>
 __device__ __forceinline__ u64p xorwow_f64p(u64p xk, u64p vk4) {
-    u64p t = xor64p(xk, shr64(xk, 2));
-    u64p r = xor64p(vk4, shl64(vk4, 4), t);
-    return xor64p(r, shl64(t, 1));
+    u64p t = xor64p(xk, shr64<2, (kF & 1) != 0>(xk));
+    u64p r = xor64p(vk4, shl64<4, (kF & 2) != 0>(vk4), t);
+    return xor64p(r, shl64<1, (kF & 4) != 0>(t));
 }
 __device__ __forceinline__ u64p add64p(u64p a, u64p b) {
     uint64_t s = ((uint64_t)a.hi << 32 | a.lo) + ((uint64_t)b.hi << 32 | b.lo);

@@ -15,6 +15,8 @@
 //    lane j of a half-warp owns streams j and j+16, one width-16 SHFL per
 //    two numbers (u[j] = tp[j] ^ tp[j+16] trick, see gen_v1.cu), and either
 //    128-bit STG or 64-stream x 32-round TMA tiles (2-D bulk tensor store).
+#include <cstdlib>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -22,8 +24,9 @@
 namespace ciprng {
 
 // Marsaglia xor64 (13, 7, 17) on (lo, hi) halves (device.cuh u64p helpers:
-// funnel halves on SHF, plain halves as IMAD.SHL / IMAD.HI).
-struct SrcXor64 {
+// plain halves as IMAD.SHL / IMAD.HI, funnel halves on SHF).
+template <int kFun>
+struct SrcXor64T {
     static constexpr int kPlanes = 2;  // a.lo, a.hi; then x, tp
     u64p a;
     __device__ __forceinline__ void load(const StateIO &io, uint64_t s) {
@@ -36,10 +39,15 @@ struct SrcXor64 {
     }
     __device__ __forceinline__ void zero() { a = {0u, 0u}; }
     __device__ __forceinline__ uint32_t next() {
-        a = xor64_step_p(a);
+        a = xor64_step_p<kFun>(a);
         return a.lo;  // Q29
     }
 };
+
+// all three funnels on SHF: multiply funnels measured slower (L2 flushed:
+// none 1.218e12, 13L 1.184e12, 13L+17L 1.083e12 numbers/s; profiles/experiments/s19)
+constexpr int kV3FunnelDefault = 0;
+using SrcXor64 = SrcXor64T<kV3FunnelDefault>;
 
 // ===================================================================== general
 template <class Src, class Sink>

@@ -14,6 +14,8 @@
 // f is Alg. 4's strategy source, t = f ^ tp[o1] ^ tp[o2]; tp = t; x ^= t
 // (P:971-974), the group's shared cells exchanged by two SHFL.IDX per number
 // (any C | 32 and any arrays; the draw, not the shuffle, is the cost here).
+#include <cstdlib>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -25,8 +27,17 @@ __device__ __forceinline__ uint32_t fold6(uint64_t t1, uint64_t t2, uint64_t t3)
            (uint32_t)t3;
 }
 
-template <class Sink, bool kComb>
+// Which funnel shifts run as multiplies (device.cuh shl64/shr64 kF), as a
+// 9-bit mask: bits 0-2 xor64 (13L, 7R, 17L), 3-5 xor128 (11L, 19R, 8R),
+// 6-8 xorwow (2R, 4L, 1L).  Measured with L2 flushed (profiles/experiments/
+// s19_funnel_summary.txt): all-SHF 4.59e11 numbers/s, 2 multiply funnels
+// 4.51e11, 6 -> 3.38e11, all 9 -> 3.26e11 -- the heavy sub-pipe costs more
+// than the ALU op it saves, so every funnel stays an SHF.
+constexpr int kFunnelDefault = 0;
+
+template <class Sink, bool kComb, int kFun = kFunnelDefault>
 __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
+    constexpr int kFunnelXor64 = kFun & 7, kFunnelXor128 = (kFun >> 3) & 7, kFunnelXorwow = (kFun >> 6) & 7;
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
@@ -82,9 +93,9 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
             uint32_t o[4];
 #pragma unroll
             for (int k = 0; k < 20; ++k) {
-                pa = xor64_step_p(pa);
-                pb[k % 4] = xor128_f64p(pb[k % 4], pb[(k + 3) % 4]);
-                pc[k % 5] = xorwow_f64p(pc[k % 5], pc[(k + 4) % 5]);
+                pa = xor64_step_p<kFunnelXor64>(pa);
+                pb[k % 4] = xor128_f64p<kFunnelXor128>(pb[k % 4], pb[(k + 3) % 4]);
+                pc[k % 5] = xorwow_f64p<kFunnelXorwow>(pc[k % 5], pc[(k + 4) % 5]);
                 pd = add64p(pd, weyl);
                 const u64p t3 = add64p(pd, pc[k % 5]);
                 update(pa.lo ^ pb[k % 4].hi ^ t3.hi ^ pb[k % 4].lo ^ pa.hi ^ t3.lo);

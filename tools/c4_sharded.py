@@ -35,7 +35,7 @@ from paper_1112_5239_b200.dist import shard_range  # noqa: E402
 def run_shards(G: int, S: int, n: int, calls: int, seed: int):
     """Digest list of `calls` calls over S streams split into G shards."""
     digests = np.zeros(calls, dtype=np.uint64)
-    gpu_s = 0.0
+    gpu_s = gen_s = 0.0
     for r in range(G):
         first, n_local = shard_range(S, G, r)
         g = P.ChaoticPRNG(seed, S, P.V1, shard=(first, n_local))
@@ -50,9 +50,17 @@ def run_shards(G: int, S: int, n: int, calls: int, seed: int):
         torch.cuda.synchronize()
         gpu_s += ev0.elapsed_time(ev1) / 1e3
         digests += P.as_u64(acc)  # uint64 wrap-around == mod 2^64
+        # generation alone (the same shard handle continues: calls+1.., work
+        # identical in shape), back-to-back launches
+        ev0.record()
+        for c in range(calls):
+            g.generate(n, out=out)
+        ev1.record()
+        torch.cuda.synchronize()
+        gen_s += ev0.elapsed_time(ev1) / 1e3
         g.close()
         del out
-    return digests, gpu_s
+    return digests, gpu_s, gen_s
 
 
 def main():
@@ -68,10 +76,12 @@ def main():
     res = {"workload": f"C4: V1, {S} streams x {n} x {calls} calls", "numbers": S * n * calls, "per_G": {}}
     ref = None
     for G in [int(x) for x in args.gpus_simulated.split(",")]:
-        d, gpu_s = run_shards(G, S, n, calls, seed)
+        d, gpu_s, gen_s = run_shards(G, S, n, calls, seed)
         same = ref is None or bool(np.array_equal(d, ref))
         ref = d if ref is None else ref
         res["per_G"][G] = {"gpu_seconds_incl_digest": gpu_s, "digests_equal_G1": same,
+                           "generate_seconds_sum_over_shards": gen_s,
+                           "generate_numbers_per_s_per_gpu": S * n * calls / gen_s,
                            "first_digests": [int(v) for v in d[:3]]}
     # oracle replay of sampled groups through all calls
     import oracle as O
