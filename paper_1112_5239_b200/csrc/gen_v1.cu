@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
             }
             i = a.n;
         } else {
-            for (; i + 4 <= a.n; i += 4) {
+            for (; i + 4 <= a.n; i += 4) {  // unroll 4 measured -1.5 % (76 regs: 6 CTAs/SM), s20
                 uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
                 CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)
                 CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)

@@ -89,3 +89,19 @@ def test_sass_has_no_tensor_core_and_has_tma_store():
     assert "UTMASTG" in sass or "UBLKCP" in sass
     assert "UTCHMMA" not in sass and "HMMA" not in sass
     assert "SHFL.IDX" in sass
+
+
+def test_next_rows_reject_bad_arguments_without_device():
+    """NEXT-2..4 entry points validate before touching the device."""
+    L = P.lib()
+    E = _lib.PRNG_EINVAL
+    assert L.prng_battery(None, 4, None, None) == E
+    assert L.prng_cbg_encrypt(1, 4, 8, None, None, None, None, None, None, None) == E
+    assert L.prng_cbg_decrypt(1, 4, 8, None, None, None, None, None, None, None, None) == E
+    assert L.prng_cbg_encrypt(1, 0, 8, None, None, None, None, None, None, None) == 0  # no messages: no-op
+    assert L.prng_alg1_generate(None, 8, 0, None, None, 4, 4, None, None) == E  # b = 0
+    assert L.prng_alg1_generate(None, 33, 4, None, None, 4, 4, None, None) == E  # n > 32
+    assert L.prng_alg1_generate(ctypes.c_void_p(16), 17, 4, None, None, 4, 4, None, None) == E  # table, n > 16
+    assert L.prng_alg1_generate(None, 8, 4, None, None, 0, 4, None, None) == 0  # no streams: no-op
+    assert L.prng_gamma_check(None, 0, None, None, None) == E
+    assert L.prng_gamma_check(None, 17, ctypes.c_void_p(16), ctypes.c_void_p(16), None) == E
