@@ -365,6 +365,10 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         if (w >= 1 && w <= 8) h->v1tune.wpb = w;
     }
     h->v1tune.l2_prefetch = env_on("CIPRNG_V1_PF", false);
+    if (const char *v = std::getenv("CIPRNG_V1_BUFS")) {
+        int b = std::atoi(v);
+        if (b >= 1 && b <= 3) h->v1tune.bufs = b;
+    }
     if (const char *v = std::getenv("CIPRNG_V1_TPW")) {
         int t = std::atoi(v);
         if (t >= 1 && t <= 64) h->v1tune.tiles_per_warp = t;

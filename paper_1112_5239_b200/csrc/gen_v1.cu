@@ -93,7 +93,7 @@ constexpr int kFastTileRows = 64;
 // kCols == 0: direct stores through the Sink (StoreSink: 128-bit STG per
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
 // TMA tile store of kCols rounds x 64 streams per box, double-buffered.
-template <class Sink, int kCols>
+template <class Sink, int kCols, int kBufs = 2>
 __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         // swizzled TMA boxes need 1 KiB-aligned shared addresses
         const uint32_t base = (smem_u32(smem_dyn) + 1023u) & ~1023u;
-        wsmem = base + (threadIdx.x >> 5) * (2 * kTileBytes);
+        wsmem = base + (threadIdx.x >> 5) * (kBufs * kTileBytes);
     }
     uint32_t tma_issued = 0;  // boxes issued by this warp
 
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
         if constexpr (kTma) {
             // boxes of kCols rounds; n % 4 == 0 guaranteed by the host
             for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
-                const uint32_t buf = wsmem + (tma_issued & 1u) * kTileBytes;
-                if (tma_issued >= 2) {
-                    if (lane == 0) bulk_wait_read<1>();
+                const uint32_t buf = wsmem + (tma_issued % kBufs) * kTileBytes;
+                if (tma_issued >= kBufs) {
+                    if (lane == 0) bulk_wait_read<kBufs - 1>();
                     __syncwarp();
                 }
                 if (i0 + kCols <= a.n) {  // full box: no per-block bound checks
@@ -394,10 +394,10 @@ static void launch_band(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles,
     launch_k(kern, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
-template <int kCols>
+template <int kCols, int kBufs = 2>
 static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, int wpb, bool pf, cudaStream_t st) {
-    const size_t smem = (size_t)wpb * 2 * kFastTileRows * kCols * 4 + 1024;  // + alignment slack
-    auto kern = v1_fast_kernel<StoreSink, kCols>;
+    const size_t smem = (size_t)wpb * kBufs * kFastTileRows * kCols * 4 + 1024;  // + alignment slack
+    auto kern = v1_fast_kernel<StoreSink, kCols, kBufs>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     GenArgs a = a0;
     // one wave of resident warps ahead (non-persistent grid: the tile the
@@ -427,6 +427,8 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
             else if (tune.cols == 128) launch_band<4, 1>(a, *tmap, tiles, wpb, tune.grid_mode, st);
             else if (tune.cols == 8) launch_fast_tma<8>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
+            else if (tune.cols == 32 && tune.bufs == 1) launch_fast_tma<32, 1>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
+            else if (tune.cols == 32 && tune.bufs == 3) launch_fast_tma<32, 3>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
             else if (tune.cols == 32) launch_fast_tma<32>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
             else launch_fast_tma<16>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
         } else {

@@ -57,3 +57,30 @@ def test_gamma_check_matches_oracle(case, n):
     assert [got["reach_from_0"], got["reach_to_0"], got["unbalanced"]] == ref.tolist()
     if case == "negation":
         assert got["chaotic"] and got["doubly_stochastic"]
+
+
+def test_theorem2_uniformity_by_sampling():
+    """Theorem 2 observed on the GPU: with Gamma(f) strongly
+    connected, Algorithm 1's outputs tend to the uniform law iff M is doubly
+    stochastic.  f = negation (doubly stochastic) gives a uniform histogram
+    over the 2^n configurations; a negation with one flipped table bit that
+    stays strongly connected but loses the degree balance (checked by the
+    oracle) gives a grossly non-uniform one."""
+    from scipy.stats import chisquare
+
+    n, V = 6, 64
+    gen = W.rng(900)
+    f_bad = ((~np.arange(V, dtype=np.uint32)) & (V - 1)).astype(np.uint32)
+    f_bad[int(gen.integers(0, V))] ^= 1 << int(gen.integers(0, n))
+    r = O.gamma_reach(f_bad, n)
+    assert int(r[0]) == V and int(r[1]) == V and int(r[2]) > 0  # chaotic, not doubly stochastic
+    S, n_out = 2**16, 64
+    p = {}
+    for name, f in (("negation", None), ("unbalanced", f_bad)):
+        z = _i32(gen.integers(1, 2**32, S).astype(np.uint32))
+        x = _i32(gen.integers(0, V, S).astype(np.uint32))
+        out = C.alg1_generate(n, 8, z, x, n_out, f=None if f is None else _i32(f))
+        # after a burn-in, every 4th output (consecutive calls share x)
+        hist = torch.bincount(out[:, 16::4].reshape(-1).long(), minlength=V).cpu().numpy()
+        p[name] = chisquare(hist).pvalue
+    assert p["negation"] > 1e-4 and p["unbalanced"] < 1e-12, p
