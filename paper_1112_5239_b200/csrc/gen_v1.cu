@@ -272,8 +272,7 @@ __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_co
     const uint32_t src = (j + 1u) & 15u;
     const uint64_t n_tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    uint32_t *P = a.state;
-    const uint64_t L = a.n_local;
+    const StateIO sio(a);
     const uint32_t rA_t = 32u * h + j, rB_t = rA_t + 16u;
     // swizzled smem offsets of this lane's two rows (row r of a band lives at
     // band*8192 + r*128, 16-byte chunk c at (c ^ (r & 7)) * 16)
@@ -293,8 +292,8 @@ __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_co
             const uint64_t sA = a.s_begin + row0 + rA_t, sB = sA + 16u;
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
-                pa[k] = P[k * L + sA];
-                pb[k] = P[k * L + sB];
+                pa[k] = sio.ld(k, sA);
+                pb[k] = sio.ld(k, sB);
             }
         }
     };
@@ -344,9 +343,10 @@ __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_co
             __syncwarp();
             if (lane == 0) {
                 asm volatile(
-                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
                         reinterpret_cast<uint64_t>(&tmap)),
-                    "r"(buf), "r"(0), "r"((int)row0), "r"((int)(i0 >> 5))
+                    "r"(buf), "r"(0), "r"((int)row0), "r"((int)(i0 >> 5)),
+                    "l"(a.evict_first ? l2_evict_first_policy() : l2_evict_normal_policy())
                     : "memory");
                 bulk_commit();
             }
@@ -357,10 +357,12 @@ __global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_co
         if (valid) {
             const uint64_t sA = a.s_begin + row0 + rA_t, sB = sA + 16u;
             // n > 0 (the host never launches n == 0): last t = g ^ nb
-            P[0 * L + sA] = a0; P[1 * L + sA] = a1; P[2 * L + sA] = a2; P[3 * L + sA] = a3;
-            P[4 * L + sA] = xA; P[5 * L + sA] = a3 ^ nb;
-            P[0 * L + sB] = b0; P[1 * L + sB] = b1; P[2 * L + sB] = b2; P[3 * L + sB] = b3;
-            P[4 * L + sB] = xB; P[5 * L + sB] = b3 ^ nb;
+            const uint32_t vA[6] = {a0, a1, a2, a3, xA, a3 ^ nb}, vB[6] = {b0, b1, b2, b3, xB, b3 ^ nb};
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                sio.st(k, sA, vA[k]);
+                sio.st(k, sB, vB[k]);
+            }
         }
     }
     if (lane == 0) bulk_wait_read<0>();  // smem must outlive the reads; global completion is ordered by the grid boundary
@@ -424,7 +426,8 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             launch_k(v1_fast_kernel<StoreSink, 0>, dim3(blocks_for(tiles, wpb, cap)), dim3(32 * wpb), 0, st, a, *tmap);
         } else if (mode == 1) {
             const int grid = blocks_for(tiles, wpb, cap);
-            if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
+            if (tune.cols == 64 && tune.bufs == 1) launch_band<2, 1>(a, *tmap, tiles, wpb, tune.grid_mode, st);
+            else if (tune.cols == 64) launch_band<2, 2>(a, *tmap, tiles, wpb, tune.grid_mode, st);
             else if (tune.cols == 128) launch_band<4, 1>(a, *tmap, tiles, wpb, tune.grid_mode, st);
             else if (tune.cols == 8) launch_fast_tma<8>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
             else if (tune.cols == 32 && tune.bufs == 1) launch_fast_tma<32, 1>(a, *tmap, grid, wpb, tune.l2_prefetch, st);
