@@ -249,6 +249,42 @@ def test_c3_full_size_two_calls():
 
 
 @pytest.mark.slow
+def test_c5_shape_consume_stats_full():
+    """BASELINE configs[4] per GPU: V1 consumer, 2^20 streams x 1024 (one GPU's
+    shard of the 2^23-stream C5 space), two calls; the 258 statistics equal
+    the oracle's over all 2^31 numbers (generated in stream chunks), and the
+    state after the calls equals the oracle's."""
+    S, n, chunk = 2**20, 1024, 2**16
+    g = P.ChaoticPRNG(SEEDS[0], S, W.V1)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        g.consume(n, stats)
+    ref = np.zeros(258, np.uint64)
+    planes = []
+    for c0 in range(0, S, chunk):
+        st = O.init_states(W.V1, SEEDS[0], c0, chunk)
+        for _ in range(2):
+            O.stats(O.generate(W.V1, st, n), ref)
+        planes.append(O.state_planes(W.V1, st))
+    got = P.as_u64(stats)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), np.concatenate(planes, axis=1))
+
+
+@pytest.mark.slow
+def test_v3_c2_shape_full_size():
+    """NEXT-1 (i) at the C2 shape: V3, 2^20 streams x 128, two calls, TMA path."""
+    S, n = 2**20, 128
+    g = P.ChaoticPRNG(SEEDS[0], S, W.V3)
+    st = O.init_states(W.V3, SEEDS[0], 0, S)
+    for _ in range(2):
+        a = P.as_u32(g.generate(n))
+        b = O.generate(W.V3, st, n)
+        assert np.array_equal(a, b), first_mismatch(a, b)
+    assert np.array_equal(g.get_state(), O.state_planes(W.V3, st))
+
+
+@pytest.mark.slow
 def test_c4_shape_sampled_groups():
     """BASELINE configs[3] shape (2^23 streams x 256 per call): 3 calls on the
     GPU, 64 sampled 32-stream groups replayed by the oracle from their own
