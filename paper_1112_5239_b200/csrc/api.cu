@@ -138,7 +138,6 @@ struct prng_s {
     uint32_t *mod = nullptr;  // V2 modulus table {M, mu} x n_mod
     uint32_t n_mod = 0;
     int num_sms = 148;
-    int persistent_blocks = 0;
     // Evict-first output stores (default; CIPRNG_EVICT_FIRST=0 disables) and an
     // optional persisting-L2 window over the state planes (CIPRNG_L2PERSIST=1;
     // measured slower than evict-first alone on B200, gpurun_out/s11).
@@ -240,7 +239,7 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
     int launches = 0;
     int path = PRNG_STORE_DIRECT;
     if (h->variant == 0) {
-        launches = launch_v0(a, mode, st, h->persistent_blocks);
+        launches = launch_v0(a, mode, st);
     } else if (h->variant == 1) {
         const bool fast = h->default_tables && h->C == 32;
         int kmode = mode;
@@ -258,9 +257,9 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
                 }
             }
         }
-        launches = launch_v1(a, fast, kmode, tm, st, h->persistent_blocks, tune);
+        launches = launch_v1(a, fast, kmode, tm, st, tune);
     } else if (h->variant == 2) {
-        launches = launch_v2(a, mode, st, h->persistent_blocks);
+        launches = launch_v2(a, mode, st);
     } else if (h->variant == 3) {
         const bool fast = h->default_tables && h->C == 32;
         int kmode = mode;
@@ -276,9 +275,9 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
                 }
             }
         }
-        launches = launch_v3(a, fast, kmode, tm, st, h->persistent_blocks);
+        launches = launch_v3(a, fast, kmode, tm, st);
     } else {
-        launches = launch_v4(a, mode, st, h->persistent_blocks);
+        launches = launch_v4(a, mode, st);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
@@ -353,7 +352,6 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         return cuda_fail(e);
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
-    h->persistent_blocks = h->num_sms * 8;
     // experiment overrides of the V1 store kernel shape
     if (const char *v = std::getenv("CIPRNG_V1_COLS")) {
         int c = std::atoi(v);

@@ -232,8 +232,7 @@ static int comb_blocks(uint64_t warps_needed, int wpb, int cap) {
 }
 
 template <class Src>
-static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-                       int persistent_blocks) {
+static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st) {
     // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
     if (a.s_count == 0) return 0;
     CUtensorMap dummy;
@@ -275,9 +274,8 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
     return 1;
 }
 
-int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks) {
-    return launch_comb<SrcXor64>(a, fast, mode, tmap, st, persistent_blocks);
+int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st) {
+    return launch_comb<SrcXor64>(a, fast, mode, tmap, st);
 }
 
 }  // namespace ciprng

@@ -145,12 +145,11 @@ __global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
 }
 
 template <bool kComb>
-static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
     const int wpb = 8;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
-    (void)persistent_blocks;
     if (mode == 2) {
         auto kern = v0_kernel<StatsSink, kComb>;
         const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
@@ -165,12 +164,12 @@ static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st, int persisten
     return 1;
 }
 
-int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
-    return launch_v0x<false>(a, mode, st, persistent_blocks);
+int launch_v0(const GenArgs &a, int mode, cudaStream_t st) {
+    return launch_v0x<false>(a, mode, st);
 }
 
-int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
-    return launch_v0x<true>(a, mode, st, persistent_blocks);
+int launch_v4(const GenArgs &a, int mode, cudaStream_t st) {
+    return launch_v0x<true>(a, mode, st);
 }
 
 }  // namespace ciprng

@@ -411,7 +411,7 @@ static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, 
 }
 
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks, const V1Tuning &tune) {
+              const V1Tuning &tune) {
     // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
     if (a.s_count == 0) return 0;
     if (fast) {

@@ -150,12 +150,11 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     sink.finish(a);
 }
 
-int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks) {
+int launch_v2(const GenArgs &a, int mode, cudaStream_t st) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
     const int wpb = 8;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
-    (void)persistent_blocks;
     if (mode == 2) {
         auto kern = v2_kernel<StatsSink>;
         const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;

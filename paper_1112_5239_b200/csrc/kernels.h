@@ -94,13 +94,12 @@ struct V1Tuning {
 
 // mode: 0 = store (direct), 1 = store (TMA tiles, V1 fast only), 2 = consume
 int launch_init(const InitArgs &a, cudaStream_t st);
-int launch_v0(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
+int launch_v0(const GenArgs &a, int mode, cudaStream_t st);
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks, const V1Tuning &tune);
-int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
-int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
-              int persistent_blocks);
-int launch_v4(const GenArgs &a, int mode, cudaStream_t st, int persistent_blocks);
+              const V1Tuning &tune);
+int launch_v2(const GenArgs &a, int mode, cudaStream_t st);
+int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st);
+int launch_v4(const GenArgs &a, int mode, cudaStream_t st);
 int launch_cbg(bool encrypt, int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *a0, const uint64_t *a1,
                const uint32_t *S0, const uint8_t *in, uint8_t *out, uint64_t *y, uint32_t *status, cudaStream_t st);
 int launch_alg1(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *z, uint32_t *x, uint64_t n_streams,
