@@ -164,3 +164,76 @@ def as_u32(t: torch.Tensor) -> np.ndarray:
 
 def as_u64(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint64)
+
+
+# ---------------------------------------------------------------------------
+# The C-ABI entry points under their own names (include/ciprng.h), for users
+# who think in the C interface; each is marshalling over the calls above.
+# ---------------------------------------------------------------------------
+def prng_create(seed: int, n_streams: int, variant: int = V1, **kw) -> ChaoticPRNG:
+    """prng_create(seed, n_streams, variant) -> handle (north_star signature)."""
+    return ChaoticPRNG(seed, n_streams, variant, **kw)
+
+
+def prng_create_shard(seed: int, first_stream: int, n_local: int, variant: int = V1, **kw) -> ChaoticPRNG:
+    return ChaoticPRNG(seed, first_stream + n_local, variant, shard=(first_stream, n_local), **kw)
+
+
+def prng_generate(h: ChaoticPRNG, n_per_stream: int, out=None, stream=None):
+    return h.generate(n_per_stream, out=out, stream=stream)
+
+
+def prng_generate_host(h: ChaoticPRNG, n_per_stream: int, out=None, stream=None):
+    return h.generate_host(n_per_stream, out=out, stream=stream)
+
+
+def prng_consume(h: ChaoticPRNG, n_per_stream: int, stats=None, stream=None):
+    return h.consume(n_per_stream, stats, stream=stream)
+
+
+def prng_battery(h: ChaoticPRNG, n_per_stream: int, stats=None, stream=None):
+    return h.battery(n_per_stream, stats, stream=stream)
+
+
+def prng_digest(out, first_stream: int = 0, acc=None, stream=None):
+    return digest(out, first_stream, acc, stream)
+
+
+def prng_get_state(h: ChaoticPRNG):
+    return h.get_state()
+
+
+def prng_set_state(h: ChaoticPRNG, planes) -> None:
+    h.set_state(planes)
+
+
+def prng_get_info(h: ChaoticPRNG):
+    return h.info()
+
+
+def prng_destroy(h: ChaoticPRNG) -> None:
+    h.close()
+
+
+def prng_cbg_encrypt(chaotic, N, r, m, S0=None, stream=None):
+    from . import bg
+
+    return bg.encrypt(chaotic, N, r, m, S0, stream)
+
+
+def prng_cbg_decrypt(chaotic, p, q, c, y, S0=None, stream=None):
+    from . import bg
+
+    return bg.decrypt(chaotic, p, q, c, y, S0, stream)
+
+
+def prng_alg1_generate(n, b, z, x, n_out, f=None, stream=None):
+    from . import chaos
+
+    return chaos.alg1_generate(n, b, z, x, n_out, f, stream)
+
+
+def prng_gamma_check(n, f=None, stream=None):
+    from . import chaos
+
+    return chaos.gamma_check(n, f, stream=stream)

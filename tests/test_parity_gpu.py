@@ -404,3 +404,16 @@ def test_cuda_graph_capture_replay():
             ref = O.generate(W.V1, st, n)
             assert np.array_equal(P.as_u32(o), ref)
     assert np.array_equal(g.get_state(), O.state_planes(W.V1, st))
+
+
+def test_abi_named_python_calls():
+    """The prng_* Python names reach the same kernels (north_star's
+    prng_create(seed, n_streams, variant) / prng_generate / prng_destroy)."""
+    h = P.prng_create(SEEDS[0], 256, W.V1)
+    a = P.as_u32(P.prng_generate(h, 40))
+    st = O.init_states(W.V1, SEEDS[0], 0, 256)
+    assert np.array_equal(a, O.generate(W.V1, st, 40))
+    s = P.as_u64(P.prng_consume(h, 8))
+    assert np.array_equal(s, O.stats(O.generate(W.V1, st, 8)))
+    assert np.array_equal(P.prng_get_state(h), O.state_planes(W.V1, st))
+    P.prng_destroy(h)
