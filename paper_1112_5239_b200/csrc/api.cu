@@ -363,6 +363,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         if (w >= 1 && w <= 8) h->v1tune.wpb = w;
     }
     h->v1tune.l2_prefetch = env_on("CIPRNG_V1_PF", false);
+    h->v1tune.smem_stg = env_on("CIPRNG_V1_SMEM_STG", false);
     if (const char *v = std::getenv("CIPRNG_V1_BUFS")) {
         int b = std::atoi(v);
         if (b >= 1 && b <= 3) h->v1tune.bufs = b;

@@ -93,7 +93,11 @@ constexpr int kFastTileRows = 64;
 // kCols == 0: direct stores through the Sink (StoreSink: 128-bit STG per
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
 // TMA tile store of kCols rounds x 64 streams per box, double-buffered.
-template <class Sink, int kCols, int kBufs = 2>
+// kStg: SURVEY s7 store path (b) -- the same swizzled shared-memory box as
+// the TMA path, written back by the warp itself with coalesced 128-bit STG
+// (8 lanes per 128-byte row piece, 4 rows per instruction) instead of a TMA
+// bulk tensor store; kept for the three-way store-path comparison.
+template <class Sink, int kCols, int kBufs = 2, bool kStg = false>
 __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
             // boxes of kCols rounds; n % 4 == 0 guaranteed by the host
             for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
                 const uint32_t buf = wsmem + (tma_issued % kBufs) * kTileBytes;
-                if (tma_issued >= kBufs) {
+                if (!kStg && tma_issued >= kBufs) {
                     if (lane == 0) bulk_wait_read<kBufs - 1>();
                     __syncwarp();
                 }
@@ -192,12 +196,34 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                 } else {
                     for (uint32_t q = 0; i0 + 4 * q < a.n; ++q) CIPRNG_V1_BLOCK4(q)
                 }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
-                    else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
-                    bulk_commit();
+                if constexpr (kStg) {
+                    // smem -> global, coalesced: lane l copies 16-byte chunk l%8 of
+                    // rows 4k + l/8 (conflict-free LDS.128 through the swizzle)
+                    static_assert(!kStg || kCols == 32, "STG staging path is for 32-round boxes");
+                    __syncwarp();
+                    const uint32_t c = lane & 7u, rsub = lane >> 3;
+                    const uint64_t cols_here = (i0 + kCols <= a.n) ? kCols : a.n - i0;
+#pragma unroll 4
+                    for (uint32_t r = rsub; r < kFastTileRows; r += 4) {
+                        const uint64_t grow = row0 + r;
+                        if (grow >= a.s_count || 4u * c >= cols_here) continue;
+                        uint32_t v0, v1, v2, v3;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                                     : "r"(buf + swz<kCols>(r, c)));
+                        uint32_t *dst = a.out + grow * a.n + i0 + 4u * c;
+                        if (a.evict_first) st_v4_cs(dst, v0, v1, v2, v3);
+                        else st_v4(dst, v0, v1, v2, v3);
+                    }
+                    __syncwarp();
+                } else {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
+                        else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
+                        bulk_commit();
+                    }
                 }
                 ++tma_issued;
             }
@@ -241,7 +267,7 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
             }
         }
     }
-    if constexpr (kTma) {
+    if constexpr (kTma && !kStg) {
         if (lane == 0) bulk_wait_read<0>();  // smem must outlive the reads; global completion is ordered by the grid boundary
         __syncwarp();
     }
@@ -396,10 +422,10 @@ static void launch_band(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles,
     launch_k(kern, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
-template <int kCols, int kBufs = 2>
+template <int kCols, int kBufs = 2, bool kStg = false>
 static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, int wpb, bool pf, cudaStream_t st) {
     const size_t smem = (size_t)wpb * kBufs * kFastTileRows * kCols * 4 + 1024;  // + alignment slack
-    auto kern = v1_fast_kernel<StoreSink, kCols, kBufs>;
+    auto kern = v1_fast_kernel<StoreSink, kCols, kBufs, kStg>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     GenArgs a = a0;
     // one wave of resident warps ahead (non-persistent grid: the tile the
@@ -422,7 +448,10 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             cap = (int)((tiles + (uint64_t)wpb * tune.tiles_per_warp - 1) / ((uint64_t)wpb * tune.tiles_per_warp));
         CUtensorMap dummy;
         if (tmap == nullptr) tmap = &dummy;
-        if (mode == 0) {
+        if (mode == 0 && tune.smem_stg && a.vec) {
+            // store path (b): shared-memory transpose + coalesced STG.128 (n % 4 == 0, aligned rows)
+            launch_fast_tma<32, 1, true>(a, *tmap, blocks_for(tiles, wpb, cap), wpb, false, st);
+        } else if (mode == 0) {
             launch_k(v1_fast_kernel<StoreSink, 0>, dim3(blocks_for(tiles, wpb, cap)), dim3(32 * wpb), 0, st, a, *tmap);
         } else if (mode == 1) {
             const int grid = blocks_for(tiles, wpb, cap);

@@ -86,6 +86,7 @@ struct V1Tuning {
     int wpb = 4;          // warps per CTA (c32 w4 0.992 vs w2 0.979 of copy peak, profiles/experiments/s16)
     int grid_blocks = 0;  // 2-D kernels: 0 = one 64-stream tile per warp, > 0 = grid cap
     int bufs = 2;            // c32: shared-memory boxes per warp (1, 2 or 3)
+    bool smem_stg = false;   // DIRECT store path via a shared-memory transpose + coalesced STG.128
     int tiles_per_warp = 1;  // 2-D kernels without a cap: grid = tiles / (wpb * tiles_per_warp)
     bool l2_prefetch = false; // 2-D TMA kernel: bulk-prefetch the next wave's state into L2 (+0.3 % flushed, -1.3 % steady: off, s18)
     int grid_mode = 0;    // band kernels: 0 = one tile per warp, -1 = persistent at

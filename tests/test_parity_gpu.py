@@ -417,3 +417,12 @@ def test_abi_named_python_calls():
     assert np.array_equal(s, O.stats(O.generate(W.V1, st, 8)))
     assert np.array_equal(P.prng_get_state(h), O.state_planes(W.V1, st))
     P.prng_destroy(h)
+
+
+def test_v1_store_path_smem_stg(monkeypatch):
+    """SURVEY s7 store path (b): the swizzled shared-memory box written back by
+    the warp with coalesced 128-bit STG -- bit-identical, incl. partial boxes,
+    a half-empty last tile and n % 4 != 0 (which falls back to the direct path)."""
+    monkeypatch.setenv("CIPRNG_V1_SMEM_STG", "1")
+    for S in (96, 4096 + 32, 65536):
+        _check(W.V1, SEEDS[2], S, [4, 36, 128, 20, 96, 160, 5], store_path=P.STORE_DIRECT)

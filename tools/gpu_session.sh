@@ -10,7 +10,8 @@ smoke) timeout 300 python __graft_entry__.py smoke > $O/smoke.log 2>&1; echo rc=
 tests) timeout 1500 python -m pytest tests -m gpu -q --maxfail=20 --timeout=900 -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo rc=$? >> $O/gpu_tests.log ;;
 fasttests) timeout 900 python -m pytest tests -m "gpu and not slow" -q --maxfail=20 --timeout=600 -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo rc=$? >> $O/gpu_tests.log ;;
 bench) timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo rc=$? >> $O/bench.err ;;
-benchpaths) for sp in 1 2; do timeout 300 python bench.py --store-path $sp --no-cpu-baseline --no-secondary --steps 400 > $O/bench_sp$sp.json 2>> $O/bench.err; done ;;
+benchpaths) for sp in 1 2; do timeout 300 python bench.py --store-path $sp --no-cpu-baseline --no-secondary --steps 400 > $O/bench_sp$sp.json 2>> $O/bench.err; done
+  CIPRNG_V1_SMEM_STG=1 timeout 300 python bench.py --store-path 1 --no-cpu-baseline --no-secondary --steps 400 > $O/bench_sp1_smemstg.json 2>> $O/bench.err ;;
 ref) timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_ref.json 2>> $O/bench.err ;;
 ncu)
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_bench_stdout.txt 2>&1

@@ -12,6 +12,9 @@ import workloads as W  # noqa: E402
 which = sys.argv[1] if len(sys.argv) > 1 else "v1"
 calls = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 seed = W.SEEDS[0]
+if which == "v1smem":
+    os.environ["CIPRNG_V1_SMEM_STG"] = "1"
+    which = "v1direct"
 if which in ("v1", "v1direct"):
     S, n = 2**20, 128
     g = P.ChaoticPRNG(seed, S, P.V1, store_path=P.STORE_DIRECT if which == "v1direct" else P.STORE_TMA)
