@@ -77,7 +77,8 @@ enum prng_status {
 
 /* Store path of prng_generate (tuning knob; every path is bit-identical). */
 enum prng_store_path {
-    PRNG_STORE_AUTO = 0,   /* TMA tiles when possible, else direct        */
+    PRNG_STORE_AUTO = 0,   /* TMA tiles when possible, else shared-memory
+                              staging + coalesced stores (V1 default tables) */
     PRNG_STORE_DIRECT = 1, /* per-thread 128-bit STG of 4-round buffers   */
     PRNG_STORE_TMA = 2     /* warp tiles staged in shared memory, written
                               by cp.async.bulk.tensor (V1 default tables,

@@ -256,6 +256,9 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
                     path = PRNG_STORE_TMA;
                 }
             }
+            // no TMA descriptor (misaligned rows, n % 4 != 0): the staged
+            // shared-memory + coalesced STG path unless DIRECT was requested
+            if (kmode == 0 && h->store_path != PRNG_STORE_DIRECT) kmode = 4;
         }
         launches = launch_v1(a, fast, kmode, tm, st, tune);
     } else if (h->variant == 2) {

@@ -183,37 +183,58 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
 
         uint64_t i = 0;
         if constexpr (kTma) {
-            // boxes of kCols rounds; n % 4 == 0 guaranteed by the host
-            for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
+            // boxes of kCols rounds over the first nb4 rounds (TMA: n % 4 == 0
+            // guaranteed by the host; staged STG: the last n % 4 rounds follow
+            // as a scalar tail)
+            const uint64_t nb4 = kStg ? (a.n & ~3ull) : a.n;
+            for (uint64_t i0 = 0; i0 < nb4; i0 += kCols) {
                 const uint32_t buf = wsmem + (tma_issued % kBufs) * kTileBytes;
                 if (!kStg && tma_issued >= kBufs) {
                     if (lane == 0) bulk_wait_read<kBufs - 1>();
                     __syncwarp();
                 }
-                if (i0 + kCols <= a.n) {  // full box: no per-block bound checks
+                if (i0 + kCols <= nb4) {  // full box: no per-block bound checks
 #pragma unroll
                     for (uint32_t q = 0; q < kCols / 4; ++q) CIPRNG_V1_BLOCK4(q)
                 } else {
-                    for (uint32_t q = 0; i0 + 4 * q < a.n; ++q) CIPRNG_V1_BLOCK4(q)
+                    for (uint32_t q = 0; i0 + 4 * q < nb4; ++q) CIPRNG_V1_BLOCK4(q)
                 }
                 if constexpr (kStg) {
-                    // smem -> global, coalesced: lane l copies 16-byte chunk l%8 of
-                    // rows 4k + l/8 (conflict-free LDS.128 through the swizzle)
                     static_assert(!kStg || kCols == 32, "STG staging path is for 32-round boxes");
                     __syncwarp();
-                    const uint32_t c = lane & 7u, rsub = lane >> 3;
-                    const uint64_t cols_here = (i0 + kCols <= a.n) ? kCols : a.n - i0;
+                    const uint64_t cols_here = (i0 + kCols <= nb4) ? kCols : nb4 - i0;
+                    if (a.vec) {
+                        // smem -> global, coalesced: lane l copies 16-byte chunk l%8 of
+                        // rows 4k + l/8 (conflict-free LDS.128 through the swizzle)
+                        const uint32_t c = lane & 7u, rsub = lane >> 3;
 #pragma unroll 4
-                    for (uint32_t r = rsub; r < kFastTileRows; r += 4) {
-                        const uint64_t grow = row0 + r;
-                        if (grow >= a.s_count || 4u * c >= cols_here) continue;
-                        uint32_t v0, v1, v2, v3;
-                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                     : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                                     : "r"(buf + swz<kCols>(r, c)));
-                        uint32_t *dst = a.out + grow * a.n + i0 + 4u * c;
-                        if (a.evict_first) st_v4_cs(dst, v0, v1, v2, v3);
-                        else st_v4(dst, v0, v1, v2, v3);
+                        for (uint32_t r = rsub; r < kFastTileRows; r += 4) {
+                            const uint64_t grow = row0 + r;
+                            if (grow >= a.s_count || 4u * c >= cols_here) continue;
+                            uint32_t v0, v1, v2, v3;
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                                         : "r"(buf + swz<kCols>(r, c)));
+                            uint32_t *dst = a.out + grow * a.n + i0 + 4u * c;
+                            if (a.evict_first) st_v4_cs(dst, v0, v1, v2, v3);
+                            else st_v4(dst, v0, v1, v2, v3);
+                        }
+                    } else {
+                        // unaligned rows (or n % 4 != 0): lane l writes word l of a
+                        // row -- 128 contiguous bytes per instruction at any
+                        // 4-byte alignment; the 32 words of a swizzled 128-byte
+                        // row sit in 32 distinct banks
+                        const uint32_t c = lane >> 2, w = lane & 3u;
+#pragma unroll 4
+                        for (uint32_t r = 0; r < kFastTileRows; ++r) {
+                            const uint64_t grow = row0 + r;
+                            if (grow >= a.s_count || lane >= cols_here) continue;
+                            uint32_t v;
+                            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(buf + swz<kCols>(r, c) + 4u * w));
+                            uint32_t *dst = a.out + grow * a.n + i0 + lane;
+                            if (a.evict_first) __stcs(dst, v);
+                            else *dst = v;
+                        }
                     }
                     __syncwarp();
                 } else {
@@ -227,7 +248,20 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                 }
                 ++tma_issued;
             }
-            i = a.n;
+            i = nb4;
+            if constexpr (kStg) {
+                for (; i < a.n; ++i) {  // the last n % 4 rounds: scalar stores
+                    uint32_t gA = xor128_f(a0, a3), gB = xor128_f(b0, b3);
+                    a0 = a1; a1 = a2; a2 = a3; a3 = gA;
+                    b0 = b1; b1 = b2; b2 = b3; b3 = gB;
+                    nb = __shfl_sync(kFull, u, src, 16);
+                    xA ^= gA ^ nb;
+                    xB ^= gB ^ nb;
+                    u = gA ^ gB;
+                    sink.put1(0, i, xA, valid);
+                    sink.put1(1, i, xB, valid);
+                }
+            }
         } else {
             for (; i + 4 <= a.n; i += 4) {  // unroll 4 measured -1.5 % (76 regs: 6 CTAs/SM), s20
                 uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
@@ -438,7 +472,7 @@ static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, 
 
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               const V1Tuning &tune) {
-    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
+    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery, 4 store staged (smem + coalesced STG)
     if (a.s_count == 0) return 0;
     if (fast) {
         const uint64_t tiles = (a.s_count + kFastTileRows - 1) / kFastTileRows;
@@ -448,8 +482,9 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             cap = (int)((tiles + (uint64_t)wpb * tune.tiles_per_warp - 1) / ((uint64_t)wpb * tune.tiles_per_warp));
         CUtensorMap dummy;
         if (tmap == nullptr) tmap = &dummy;
-        if (mode == 0 && tune.smem_stg && a.vec) {
-            // store path (b): shared-memory transpose + coalesced STG.128 (n % 4 == 0, aligned rows)
+        if (mode == 4 || (mode == 0 && tune.smem_stg)) {
+            // store path (b): shared-memory transpose + coalesced STG (any alignment, any n);
+            // mode 4 = the AUTO fallback when no TMA descriptor applies
             launch_fast_tma<32, 1, true>(a, *tmap, blocks_for(tiles, wpb, cap), wpb, false, st);
         } else if (mode == 0) {
             launch_k(v1_fast_kernel<StoreSink, 0>, dim3(blocks_for(tiles, wpb, cap)), dim3(32 * wpb), 0, st, a, *tmap);
