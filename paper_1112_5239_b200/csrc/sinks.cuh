@@ -16,10 +16,12 @@ struct StoreSink {
     uint64_t n;
     bool vec, cs;       // cs: L2 evict-first (streaming) stores
     uint32_t *base[2];  // row start of each of the lane's (up to two) streams
-    // streaming stores only pay together with L2-resident state (small planes):
-    // with V4's 96 MiB of state STG.EF measured 10 % slower (gpurun_out/s14)
+    // Per-lane stores are 16-byte pieces of rows n*4 bytes apart: L2 must hold
+    // each line until its other pieces arrive, so an evict-first hint here
+    // forces partial-sector read-modify-writes (V1 direct: 293 MB of DRAM
+    // reads per launch, profiles/experiments/s27) -- plain stores only.
     __device__ __forceinline__ explicit StoreSink(const GenArgs &a)
-        : out(a.out), n(a.n), vec(a.vec != 0), cs(a.evict_first != 0 && a.state_last != 0) {}
+        : out(a.out), n(a.n), vec(a.vec != 0), cs(false) {}
     // slot: which of the lane's streams (the V1 fast kernel owns two)
     __device__ __forceinline__ void begin_row(int slot, uint64_t row) { base[slot] = out + row * n; }
     __device__ __forceinline__ void put4(int slot, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2,
