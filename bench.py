@@ -336,13 +336,16 @@ def run_ours(args):
     steady_ms = float(t.item())
     steady_value = numbers / (steady_ms / 1e3)
 
-    # (3) the same steady state replayed from a CUDA graph of 10 calls
+    # (3) the same steady state replayed from a CUDA graph of 10 calls (single
+    # process only: a capture must not race the NCCL watchdog thread)
     graph_value = None
     try:
+        if ws > 1:
+            raise RuntimeError("skipped under torch.distributed")
         gs = torch.cuda.Stream()
         gs.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=gs):
+        with torch.cuda.graph(graph, stream=gs, capture_error_mode="thread_local"):
             for _ in range(10):
                 g.generate(n, out=out)
         reps = max(1, args.steps // 10)
