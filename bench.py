@@ -266,11 +266,18 @@ def run_ours(args):
     import paper_1112_5239_b200 as P
 
     rank, ws, lr = env_rank()
+    # one process per GPU; CIPRNG_BENCH_BACKEND=gloo lets tests drive the
+    # multi-rank path with several ranks on one GPU (device = local rank mod #GPUs)
+    lr = lr % max(1, torch.cuda.device_count())
     if ws > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(lr)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        backend = os.environ.get("CIPRNG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(lr)
         dist = None

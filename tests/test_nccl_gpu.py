@@ -40,3 +40,21 @@ def test_torchrun_nccl_consume_matches_oracle(variant):
     for _ in range(calls):
         O.stats(O.generate(variant, st, n), ref)
     assert got == [int(v) for v in ref]
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py's torchrun (N > 1) code path end to end: two ranks sharing the
+    one GPU here over gloo (the driver's N-GPU runs use NCCL, one GPU each).
+    Rank 0 alone prints one JSON line; the stream space is the union of both
+    shards; timing is the max over ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "6", "--warmup", "3", "--streams", "65536", "--no-secondary", "--e2e-steps", "1"]
+    env = dict(os.environ, CIPRNG_BENCH_BACKEND="gloo")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_streams"] == 2 * 65536 and d["value"] > 0
+    assert d["scaling"] == "weak" and "cpu_baseline" not in d
