@@ -277,6 +277,7 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
                     path = PRNG_STORE_TMA;
                 }
             }
+            if (kmode == 0 && h->store_path != PRNG_STORE_DIRECT) kmode = 4;  // staged fallback
         }
         launches = launch_v3(a, fast, kmode, tm, st);
     } else {

@@ -179,6 +179,45 @@ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) {
     return r * P + ((c ^ ((r * P >> 7) & (P / 16 - 1))) << 4);
 }
 
+// Write a warp's swizzled shared-memory box (64 rows x kCols words, rows
+// 0..63 of the tile at row0, rounds i0..i0+cols) to out[row * n + round]
+// with coalesced stores -- the staged store path (no TMA descriptor needed):
+// rows 16-byte aligned (vec): lane l moves 16-byte chunk l%8 of rows 4k+l/8
+// (STG.128, 4 rows per instruction); otherwise lane l moves word l of one
+// row (128 contiguous bytes per instruction at any 4-byte alignment).  Both
+// read the swizzled box bank-conflict-free.
+template <int kCols>
+__device__ __forceinline__ void staged_writeback(uint32_t buf, uint32_t *out, uint64_t row0, uint64_t rows_valid,
+                                                 uint64_t n, uint64_t i0, uint64_t cols, bool vec, bool cs,
+                                                 uint32_t lane) {
+    static_assert(kCols == 32, "staged write-back is for 32-round boxes");
+    if (vec) {
+        const uint32_t c = lane & 7u, rsub = lane >> 3;
+#pragma unroll 4
+        for (uint32_t r = rsub; r < 64u; r += 4) {
+            if (row0 + r >= rows_valid || 4u * c >= cols) continue;
+            uint32_t v0, v1, v2, v3;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                         : "r"(buf + swz<kCols>(r, c)));
+            uint32_t *dst = out + (row0 + r) * n + i0 + 4u * c;
+            if (cs) st_v4_cs(dst, v0, v1, v2, v3);
+            else st_v4(dst, v0, v1, v2, v3);
+        }
+    } else {
+        const uint32_t c = lane >> 2, w = lane & 3u;
+#pragma unroll 4
+        for (uint32_t r = 0; r < 64u; ++r) {
+            if (row0 + r >= rows_valid || lane >= cols) continue;
+            uint32_t v;
+            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(buf + swz<kCols>(r, c) + 4u * w));
+            uint32_t *dst = out + (row0 + r) * n + i0 + lane;
+            if (cs) __stcs(dst, v);
+            else *dst = v;
+        }
+    }
+}
+
 // ------------------------------------------- programmatic dependent launch
 // Every kernel is launched with programmatic stream serialization (PDL): it
 // lets the next kernel on the stream be scheduled while this one drains, and

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
 // ======================================================================== fast
 constexpr int kCombTileRows = 64;
 
-template <class Src, class Sink, int kCols>
+template <class Src, class Sink, int kCols, bool kStg = false>
 __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int X = Src::kPlanes, TP = Src::kPlanes + 1;
     constexpr bool kTma = kCols > 0;
@@ -161,13 +161,16 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
         };
         uint64_t i = 0;
         if constexpr (kTma) {
-            for (uint64_t i0 = 0; i0 < a.n; i0 += kCols) {
+            // staged store path (kStg): boxes over the first n - n%4 rounds,
+            // scalar tail after; TMA: n % 4 == 0 (host)
+            const uint64_t nb4 = kStg ? (a.n & ~3ull) : a.n;
+            for (uint64_t i0 = 0; i0 < nb4; i0 += kCols) {
                 const uint32_t buf = wsmem + (issued & 1u) * kTileBytes;
-                if (issued >= 2) {
+                if (!kStg && issued >= 2) {
                     if (lane == 0) bulk_wait_read<1>();
                     __syncwarp();
                 }
-                const uint32_t q_end = (i0 + kCols <= a.n) ? kCols / 4 : (uint32_t)((a.n - i0) / 4);
+                const uint32_t q_end = (i0 + kCols <= nb4) ? kCols / 4 : (uint32_t)((nb4 - i0) / 4);
 #pragma unroll 8
                 for (uint32_t q = 0; q < q_end; ++q) {
                     uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
@@ -178,16 +181,32 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
                     st_shared_v4(buf + swz<kCols>(rA_t, q), oA0, oA1, oA2, oA3);
                     st_shared_v4(buf + swz<kCols>(rB_t, q), oB0, oB1, oB2, oB3);
                 }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
-                    else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
-                    bulk_commit();
+                if constexpr (kStg) {
+                    __syncwarp();
+                    staged_writeback<kCols>(buf, a.out, row0, a.s_count, a.n, i0,
+                                            (i0 + kCols <= nb4) ? kCols : nb4 - i0, a.vec != 0,
+                                            a.evict_first != 0, lane);
+                    __syncwarp();
+                } else {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (a.evict_first) tma_store_2d_hint(&tmap, buf, (int)i0, (int)row0, l2_evict_first_policy());
+                        else tma_store_2d(&tmap, buf, (int)i0, (int)row0);
+                        bulk_commit();
+                    }
                 }
                 ++issued;
             }
-            i = a.n;
+            i = nb4;
+            if constexpr (kStg) {
+                for (; i < a.n; ++i) {  // the last n % 4 rounds: scalar stores
+                    uint32_t oA, oB;
+                    round2(oA, oB);
+                    sink.put1(0, i, oA, valid);
+                    sink.put1(1, i, oB, valid);
+                }
+            }
         } else {
             for (; i + 4 <= a.n; i += 4) {
                 uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
@@ -217,7 +236,7 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
             sio.st(X, sB, xB); sio.st(TP, sB, tpB);
         }
     }
-    if constexpr (kTma) {
+    if constexpr (kTma && !kStg) {
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
     }
@@ -233,13 +252,19 @@ static int comb_blocks(uint64_t warps_needed, int wpb, int cap) {
 
 template <class Src>
 static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st) {
-    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery
+    // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery, 4 store staged
     if (a.s_count == 0) return 0;
     CUtensorMap dummy;
     if (tmap == nullptr) tmap = &dummy;
     if (fast) {
         const uint64_t tiles = (a.s_count + kCombTileRows - 1) / kCombTileRows;
-        if (mode == 1) {
+        if (mode == 4) {  // staged shared-memory + coalesced STG (no TMA descriptor)
+            constexpr int kCols = 32, wpb = 2;
+            const size_t smem = (size_t)wpb * 2 * kCombTileRows * kCols * 4 + 1024;
+            auto kern = comb_fast_kernel<Src, StoreSink, kCols, true>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            launch_k(kern, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), smem, st, a, *tmap);
+        } else if (mode == 1) {
             constexpr int kCols = 32, wpb = 2;  // V3: wpb 4 measured 1.5 % slower (profiles/experiments/s18)
             const size_t smem = (size_t)wpb * 2 * kCombTileRows * kCols * 4 + 1024;
             auto kern = comb_fast_kernel<Src, StoreSink, kCols>;

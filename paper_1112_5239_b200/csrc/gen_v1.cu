@@ -200,42 +200,10 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                     for (uint32_t q = 0; i0 + 4 * q < nb4; ++q) CIPRNG_V1_BLOCK4(q)
                 }
                 if constexpr (kStg) {
-                    static_assert(!kStg || kCols == 32, "STG staging path is for 32-round boxes");
                     __syncwarp();
-                    const uint64_t cols_here = (i0 + kCols <= nb4) ? kCols : nb4 - i0;
-                    if (a.vec) {
-                        // smem -> global, coalesced: lane l copies 16-byte chunk l%8 of
-                        // rows 4k + l/8 (conflict-free LDS.128 through the swizzle)
-                        const uint32_t c = lane & 7u, rsub = lane >> 3;
-#pragma unroll 4
-                        for (uint32_t r = rsub; r < kFastTileRows; r += 4) {
-                            const uint64_t grow = row0 + r;
-                            if (grow >= a.s_count || 4u * c >= cols_here) continue;
-                            uint32_t v0, v1, v2, v3;
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                                         : "r"(buf + swz<kCols>(r, c)));
-                            uint32_t *dst = a.out + grow * a.n + i0 + 4u * c;
-                            if (a.evict_first) st_v4_cs(dst, v0, v1, v2, v3);
-                            else st_v4(dst, v0, v1, v2, v3);
-                        }
-                    } else {
-                        // unaligned rows (or n % 4 != 0): lane l writes word l of a
-                        // row -- 128 contiguous bytes per instruction at any
-                        // 4-byte alignment; the 32 words of a swizzled 128-byte
-                        // row sit in 32 distinct banks
-                        const uint32_t c = lane >> 2, w = lane & 3u;
-#pragma unroll 4
-                        for (uint32_t r = 0; r < kFastTileRows; ++r) {
-                            const uint64_t grow = row0 + r;
-                            if (grow >= a.s_count || lane >= cols_here) continue;
-                            uint32_t v;
-                            asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(buf + swz<kCols>(r, c) + 4u * w));
-                            uint32_t *dst = a.out + grow * a.n + i0 + lane;
-                            if (a.evict_first) __stcs(dst, v);
-                            else *dst = v;
-                        }
-                    }
+                    staged_writeback<kCols>(buf, a.out, row0, a.s_count, a.n, i0,
+                                            (i0 + kCols <= nb4) ? kCols : nb4 - i0, a.vec != 0,
+                                            a.evict_first != 0, lane);
                     __syncwarp();
                 } else {
                     fence_proxy_async_smem();
