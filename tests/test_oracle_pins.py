@@ -484,3 +484,16 @@ def test_v34_seeding():
     assert np.array_equal(v4[:, :22], v0[:, :22])
     assert v4[:, 22].tolist() == [O.splitmix_word(5, s, 11) & M32 for s in (7, 8)]
     assert v4[:, 23].tolist() == [O.splitmix_word(5, s, 12) & M32 for s in (7, 8)]
+
+
+def test_survey_vectors(golden):
+    """SURVEY.md Appendix A's independently computed vectors (see the golden
+    file's note): generator prefixes and Listing 1's first outputs."""
+    g = golden["survey_vectors"]
+    assert O.xor64_seq(g["xor64_first3"]["seed"], 3) == g["xor64_first3"]["outputs"]
+    assert O.xor128_32_seq(g["xor128_32_first5"]["seed"], 5) == g["xor128_32_first5"]["outputs"]
+    assert O.xor128_64_seq(g["xor128_64_first2"]["seed"], 2) == g["xor128_64_first2"]["outputs"]
+    e = g["xorwow_64_first2"]
+    assert O.xorwow_64_seq(e["seed"], e["d"], 2) == e["outputs"] == e["published_32bit_xorwow"][:2]
+    st = O.init_states(O.V0, 0, 0, 1, paper_defaults=True)
+    assert O.generate(O.V0, st, 4)[0].tolist() == g["listing1_paper_defaults_first4"]["outputs"]
