@@ -4,8 +4,8 @@
 Metric (BASELINE.json): 32-bit random numbers/s, whole job, and the fraction
 of the HBM write roofline.  One step = one prng_generate call of BASELINE
 configs[1] per GPU: V1 (Alg. 4, xor128 + neighbour combination), 2^20 streams
-x 128 numbers, stored to HBM (512 MiB per step, > 126 MB L2, so no L2 flush
-is needed).  Multi-GPU (torchrun, one process per GPU): every rank owns 2^20
+x 128 numbers, stored to HBM (512 MiB per step); L2 is flushed (untimed)
+before every timed call so the 24 MiB of state start each call in HBM.  Multi-GPU (torchrun, one process per GPU): every rank owns 2^20
 consecutive streams of one global stream space (weak scaling); the store path
 has no collective at all.
 
@@ -260,6 +260,27 @@ def run_reference(args):
     return 0
 
 
+class L2Flush:
+    """Untimed L2 flush between timed calls: a 256 MiB write (> the 126 MB
+    L2) followed by a 256 MiB read.  The write alone leaves up to ~126 MB of
+    the flush buffer's own DIRTY lines in L2, whose write-back to HBM would
+    then land inside the next timed call (measured: write-only flush 1.484e12
+    vs write+read 1.51-1.53e12 numbers/s, tools/exp_flush.py,
+    profiles/experiments/s32_flush.json); the read pass writes them back
+    before the timer starts and leaves L2 full of clean, unrelated lines, so
+    the timed call still finds its state planes in HBM."""
+
+    def __init__(self, torch, dev):
+        self.w = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
+        self.r = torch.ones(64 * 2**20, dtype=torch.int32, device=dev)
+        self.acc = torch.empty((), dtype=torch.int64, device=dev)
+        self.torch = torch
+
+    def __call__(self, k: int) -> None:
+        self.w.fill_(k)
+        self.acc.copy_(self.r.sum(dtype=self.torch.int64))
+
+
 def run_ours(args):
     import torch
 
@@ -297,17 +318,17 @@ def run_ours(args):
     store_path_used = g.info().store_path
     torch.cuda.synchronize()
 
-    # (1) headline: L2 flushed between timed steps (a 256 MiB write > the 126
+    # (1) headline: L2 flushed between timed steps (L2Flush: 256 MiB write + read > the 126
     # MB L2 before every call, outside the timed interval), each call timed
     # with CUDA events on the launching stream -- the state planes (24 MiB)
     # start every call in HBM.
-    scratch = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
+    flush = L2Flush(torch, dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(lr) as clk:
         for k in range(args.steps):
-            scratch.fill_(k)
+            flush(k)
             ev[k][0].record(stream)
             g.generate(n, out=out)
             ev[k][1].record(stream)
@@ -320,7 +341,7 @@ def run_ours(args):
     total_ms = float(t.item())
     numbers = args.steps * S * n * ws
     value = numbers / (total_ms / 1e3)
-    del scratch
+    del flush
 
     # (2) steady state: back-to-back calls with no flush (no per-launch events:
     # they would break the programmatic-dependent-launch overlap).  The output
@@ -427,7 +448,7 @@ def run_ours(args):
             "n_per_stream": n,
             "global_streams": S * ws,
             "store_path": {1: "direct", 2: "tma"}.get(store_path_used, str(store_path_used)),
-            "l2": "L2 flushed before every timed step (256 MiB write, untimed); output "
+            "l2": "L2 flushed before every timed step (256 MiB write then 256 MiB read, untimed); output "
                   f"{4 * S * n >> 20} MiB per step per GPU, state {STATE_BYTES_V1 * S >> 20} MiB",
             "parallelism": f"stream-sharded x{ws} (no collective on the store path)",
         },
@@ -501,7 +522,7 @@ def measure_secondary(P, torch, dev, args):
     res = {}
     stream = torch.cuda.current_stream()
 
-    scratch = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
+    flush = L2Flush(torch, dev)
 
     def timed(fn, steps):
         """mean seconds per call; L2 flushed (untimed) before every call."""
@@ -510,7 +531,7 @@ def measure_secondary(P, torch, dev, args):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         torch.cuda.synchronize()
         for k in range(steps):
-            scratch.fill_(k)
+            flush(k)
             ev[k][0].record(stream)
             fn()
             ev[k][1].record(stream)

@@ -302,11 +302,18 @@ CIPRNG_API int prng_set_state(prng_t *h, const void *host_buf, size_t bytes);
 CIPRNG_API const char *prng_strerror(int status);
 CIPRNG_API const char *prng_last_cuda_error(void);
 
-/* Host-side exhaustive self-check of the kernels' division-free BBS squaring
- * (Barrett, P:1209-1211 asks for 32-bit modulus only): for every modulus of
- * the table and every y < M, compares with y*y % M.  Writes the number of
- * mismatches; runs on the CPU (no GPU needed). */
+/* Host-side exhaustive self-check of the kernels' division-free BBS squarings
+ * (P:1209-1211 asks for 32-bit modulus arithmetic only): for every modulus
+ * of the table and every y < M, compares Barrett (IMAD.HI quotient) and the
+ * FP32-quotient form (host emulation of its round-toward-zero steps) with
+ * y*y % M.  Writes the number of mismatches; runs on the CPU (no GPU). */
 CIPRNG_API int prng_selftest_modsq(uint64_t *mismatches);
+
+/* The same exhaustive check executed by a kernel on the current device (the
+ * FP32 rounding itself is then the hardware's).  Synchronous; allocates and
+ * frees its own device buffers.  Returns PRNG_ECUDA on a CUDA failure (e.g.
+ * no GPU), PRNG_EINVAL for a null pointer. */
+CIPRNG_API int prng_selftest_modsq_gpu(uint64_t *mismatches);
 
 /* Library build string (compiler, arch). */
 CIPRNG_API const char *prng_version(void);

@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
             "prng_strerror": ([i32], ctypes.c_char_p),
             "prng_last_cuda_error": ([], ctypes.c_char_p),
             "prng_selftest_modsq": ([ctypes.POINTER(u64)], i32),
+            "prng_selftest_modsq_gpu": ([ctypes.POINTER(u64)], i32),
             "prng_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():

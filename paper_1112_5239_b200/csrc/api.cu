@@ -47,9 +47,20 @@ struct DeviceGuard {
 
 // Modulus table of V2 (reading Q13), built here independently of any other
 // component: primes p = 3 (mod 4) in [128, 256] by a sieve, products p < q
-// ascending, each as one 16-byte entry {M, mu = floor(2^32 / M), 2^32 - M, 0}
-// (one 128-bit load per BBS instance; the negated modulus is stored rather
-// than derived so the kernel's Barrett step stays 3 IMAD + 1 VIADDMNMX).
+// ascending, each as one 32-byte entry (kModWords words)
+//   {invMf = bits of RZ(1/M) as float, mu = floor(2^32 / M), 2^32 - M,
+//    K = 0x4B000000 * M mod 2^32, M, 0, 0, 0}
+// so one 128-bit load gives a BBS instance everything both squarings need
+// (barrett_sq: mu, 2^32 - M; fbarrett_sq: invMf, 2^32 - M, K; device.cuh);
+// the negated modulus is stored rather than derived so each squaring ends in
+// one IMAD + one VIADDMNMX.
+static uint32_t rz_recip_bits(uint32_t M) {
+    int k = 0;  // 2^23 <= floor(2^k / M) < 2^24: then RZ(1/M) = floor(2^k / M) * 2^-k
+    while (((1ull << k) / M) < (1ull << 23)) ++k;
+    const uint32_t m = (uint32_t)((1ull << k) / M);
+    return ((uint32_t)(127 + 23 - k) << 23) | (m & 0x7FFFFFu);
+}
+
 std::vector<uint32_t> modulus_table() {
     std::vector<bool> composite(257, false);
     std::vector<uint32_t> primes;
@@ -64,10 +75,9 @@ std::vector<uint32_t> modulus_table() {
     std::sort(Ms.begin(), Ms.end());
     std::vector<uint32_t> tab;
     for (uint32_t M : Ms) {
-        tab.push_back(M);
-        tab.push_back((uint32_t)((1ull << 32) / M));
-        tab.push_back(0u - M);
-        tab.push_back(0u);
+        const uint32_t e[kModWords] = {rz_recip_bits(M), (uint32_t)((1ull << 32) / M), 0u - M,
+                                       0x4B000000u * M, M, 0u, 0u, 0u};
+        tab.insert(tab.end(), e, e + kModWords);
     }
     return tab;
 }
@@ -135,7 +145,7 @@ struct prng_s {
     int store_path = PRNG_STORE_AUTO;
     CombTables comb{};
     uint32_t *state = nullptr;
-    uint32_t *mod = nullptr;  // V2 modulus table {M, mu} x n_mod
+    uint32_t *mod = nullptr;  // V2 modulus table, n_mod entries of kModWords words
     uint32_t n_mod = 0;
     int num_sms = 148;
     // Evict-first output stores (default; CIPRNG_EVICT_FIRST=0 disables) and an
@@ -146,6 +156,7 @@ struct prng_s {
     bool evict_first = true;
     bool state_last = true;
     V1Tuning v1tune;
+    int v2_kind = -1;  // V2 store kernel instantiation (CIPRNG_V2_KIND, experiments; -1 = default)
     // last call info
     int last_path = 0;
     uint32_t last_launches = 0;
@@ -262,7 +273,7 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
         }
         launches = launch_v1(a, fast, kmode, tm, st, tune);
     } else if (h->variant == 2) {
-        launches = launch_v2(a, mode, st);
+        launches = launch_v2(a, mode, st, h->v2_kind);
     } else if (h->variant == 3) {
         const bool fast = h->default_tables && h->C == 32;
         int kmode = mode;
@@ -366,6 +377,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         int w = std::atoi(v);
         if (w >= 1 && w <= 8) h->v1tune.wpb = w;
     }
+    if (const char *v = std::getenv("CIPRNG_V2_KIND")) h->v2_kind = std::atoi(v);
     h->v1tune.l2_prefetch = env_on("CIPRNG_V1_PF", false);
     h->v1tune.smem_stg = env_on("CIPRNG_V1_SMEM_STG", false);
     if (const char *v = std::getenv("CIPRNG_V1_BUFS")) {
@@ -414,7 +426,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         cudaGetLastError();  // the policy is an optimisation: never fail creation on it
     }
     std::vector<uint32_t> tab = modulus_table();
-    h->n_mod = (uint32_t)(tab.size() / 4);
+    h->n_mod = (uint32_t)(tab.size() / kModWords);
     e = cudaMalloc(&h->mod, tab.size() * 4);
     if (e == cudaSuccess) e = cudaMemcpy(h->mod, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -657,13 +669,38 @@ int prng_selftest_modsq(uint64_t *mismatches) {
     if (!mismatches) return PRNG_EINVAL;
     std::vector<uint32_t> tab = modulus_table();
     uint64_t bad = 0;
-    for (size_t k = 0; k + 3 < tab.size(); k += 4) {
-        const uint32_t M = tab[k], mu = tab[k + 1], nM = tab[k + 2];
-        if (nM != 0u - M) ++bad;
-        for (uint32_t y = 0; y < M; ++y)
-            if (barrett_sq(y, nM, mu) != (y * y) % M) ++bad;
+    for (size_t k = 0; k + kModWords <= tab.size(); k += kModWords) {
+        const uint32_t invMf = tab[k], mu = tab[k + 1], nM = tab[k + 2], K = tab[k + 3], M = tab[k + 4];
+        if (nM != 0u - M || K != 0x4B000000u * M) ++bad;
+        for (uint32_t y = 0; y < M; ++y) {
+            const uint32_t ref = (y * y) % M;
+            if (barrett_sq(y, nM, mu) != ref) ++bad;
+            if (fbarrett_sq(y, nM, K, invMf) != ref) ++bad;
+        }
     }
     *mismatches = bad;
+    return PRNG_OK;
+}
+
+int prng_selftest_modsq_gpu(uint64_t *mismatches) {
+    if (!mismatches) return PRNG_EINVAL;
+    std::vector<uint32_t> tab = modulus_table();
+    uint32_t *mod = nullptr;
+    unsigned long long *bad = nullptr;
+    cudaError_t e = cudaMalloc(&mod, tab.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemcpy(mod, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(bad, 0, sizeof(unsigned long long));
+    if (e == cudaSuccess) {
+        launch_modsq_check(mod, (uint32_t)(tab.size() / kModWords), bad, 0);
+        e = cudaGetLastError();
+    }
+    unsigned long long host = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&host, bad, sizeof(host), cudaMemcpyDeviceToHost);
+    cudaFree(mod);
+    cudaFree(bad);
+    if (e != cudaSuccess) return cuda_fail(e);
+    *mismatches = host;
     return PRNG_OK;
 }
 

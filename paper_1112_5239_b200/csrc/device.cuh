@@ -87,6 +87,42 @@ __host__ __device__ __forceinline__ uint32_t barrett_sq(uint32_t y, uint32_t nM,
     return r2 < r ? r2 : r;
 }
 
+// The same squaring with the quotient taken from the FP32 pipe, which runs
+// beside the heavy FMA sub-pipe (IMAD + FFMA interleaved: 118 lane-ops/clk/SM,
+// profiles/r1e_pipe_microbench.json), so the half-rate IMAD.HI leaves the
+// bound pipe: 2 IMAD (4 heavy cycles) instead of IMAD + IMAD.HI + IMAD (8).
+//   yf = y exactly (y < 2^23: magic-exponent conversion, LOP3 + FADD)
+//   Tf = RZ(y*y)              relative error < 2^-23, Tf <= y^2
+//   invMf = RZ(1/M)           relative error < 2^-23, invMf <= 1/M
+//   qb = RZ(Tf*invMf + 2^23)  one FFMA: the exact product, one rounding; the
+//        sum lies in [2^23, 2^24) where RZ = floor, so bits(qb) = 0x4B000000
+//        + floor(Tf*invMf), and y^2/M - Tf*invMf < 2^-22 * y^2/M < 2^-6
+//        gives floor(Tf*invMf) in {q - 1, q}, q = floor(y^2 / M).
+//   r = y*y + K + bits(qb)*(2^32 - M) = y^2 - q_est*M (mod 2^32), with
+//        K = 0x4B000000 * M mod 2^32 cancelling the exponent bits; r < 2M,
+//        so the same unsigned-min subtraction finishes.
+// Exhaustively checked against % by prng_selftest_modsq() (host emulation
+// below, bit-exact by construction) and by the GPU test of every modulus
+// and every y < M through the kernel itself.
+__host__ __device__ __forceinline__ uint32_t fbarrett_sq(uint32_t y, uint32_t nM, uint32_t K, uint32_t invMf) {
+#ifdef __CUDA_ARCH__
+    const float yf = __uint_as_float(y | 0x4B000000u) - 8388608.0f;
+    const float Tf = __fmul_rz(yf, yf);
+    const uint32_t qb = __float_as_uint(__fmaf_rz(Tf, __uint_as_float(invMf), 8388608.0f));
+#else
+    uint64_t T = (uint64_t)y * y;  // RZ to 24 significant bits
+    int bl = 0;
+    while (bl < 64 && (T >> bl)) ++bl;
+    if (bl > 24) T = (T >> (bl - 24)) << (bl - 24);
+    const uint64_t m = (invMf & 0x7FFFFFu) | 0x800000u;           // invMf = m * 2^-e
+    const int e = 127 + 23 - (int)((invMf >> 23) & 0xFFu);           // e in (23, 64) here
+    const uint32_t qb = 0x4B000000u + (uint32_t)((T * m) >> e);     // T*m < 2^56
+#endif
+    const uint32_t r = y * y + K + qb * nM;
+    const uint32_t r2 = r + nM;
+    return r2 < r ? r2 : r;
+}
+
 // ---------------------------------------------------------------- stores
 __device__ __forceinline__ void st_v4(uint32_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)

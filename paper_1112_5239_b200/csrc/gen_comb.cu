@@ -274,11 +274,11 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
             launch_k(comb_fast_kernel<Src, StoreSink, 0>, dim3(comb_blocks(tiles, 4, 0)), dim3(128), 0, st, a, *tmap);
         } else if (mode == 2) {
             auto kern = comb_fast_kernel<Src, StatsSink, 0>;
-            const size_t sm = 4 * StatsSink::kSmemBytesPerWarp;
+            const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);
         } else {
             auto kern = comb_fast_kernel<Src, BatterySink, 0>;
-            const size_t sm = 4 * BatterySink::kSmemBytesPerWarp;
+            const size_t sm = 4 * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);
         }
     } else {
@@ -286,11 +286,11 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
         const int wpb = 8;
         if (mode == 2) {
             auto kern = comb_general_kernel<Src, StatsSink>;
-            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, (tiles + wpb - 1) / wpb)), dim3(32 * wpb), sm, st, a);
         } else if (mode == 3) {
             auto kern = comb_general_kernel<Src, BatterySink>;
-            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, (tiles + wpb - 1) / wpb)), dim3(32 * wpb), sm, st, a);
         } else {
             launch_k(comb_general_kernel<Src, StoreSink>, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), 0, st, a);

@@ -152,11 +152,11 @@ static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st) {
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         auto kern = v0_kernel<StatsSink, kComb>;
-        const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+        const size_t sm = wpb * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else if (mode == 3) {
         auto kern = v0_kernel<BatterySink, kComb>;
-        const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+        const size_t sm = wpb * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else {
         launch_k(v0_kernel<StoreSink, kComb>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);

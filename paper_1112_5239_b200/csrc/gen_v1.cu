@@ -231,15 +231,27 @@ __global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_co
                 }
             }
         } else {
-            for (; i + 4 <= a.n; i += 4) {  // unroll 4 measured -1.5 % (76 regs: 6 CTAs/SM), s20
-                uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
-                CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)
-                CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)
-                CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)
-                CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)
-                sink.put4(0, i, oA0, oA1, oA2, oA3, valid);
-                sink.put4(1, i, oB0, oB1, oB2, oB3, valid);
+#define CIPRNG_V1_DIRECT4(I)                              \
+    {                                                     \
+        uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;  \
+        CIPRNG_V1_ROUND(a0, a3, b0, b3, oA0, oB0)         \
+        CIPRNG_V1_ROUND(a1, a0, b1, b0, oA1, oB1)         \
+        CIPRNG_V1_ROUND(a2, a1, b2, b1, oA2, oB2)         \
+        CIPRNG_V1_ROUND(a3, a2, b3, b2, oA3, oB3)         \
+        sink.put4(0, (I), oA0, oA1, oA2, oA3, valid);     \
+        sink.put4(1, (I), oB0, oB1, oB2, oB3, valid);     \
+    }
+            // unroll 4 (8 rounds measured -1.5 %: 76 regs, 6 CTAs/SM, s20)
+            if constexpr (Sink::kStats) {
+                // consumers: n < 2^24 (host-checked), a 32-bit trip counter
+                // and index (the u64 loop against a.n cost 8 instructions per 4 rounds)
+                const uint32_t n4 = (uint32_t)a.n & ~3u;
+                for (uint32_t i32 = 0; i32 != n4; i32 += 4) CIPRNG_V1_DIRECT4(i32)
+                i = n4;
+            } else {
+                for (; i + 4 <= a.n; i += 4) CIPRNG_V1_DIRECT4(i)
             }
+#undef CIPRNG_V1_DIRECT4
             for (; i < a.n; ++i) {  // ragged tail
                 uint32_t gA = xor128_f(a0, a3), gB = xor128_f(b0, b3);
                 a0 = a1; a1 = a2; a2 = a3; a3 = gA;
@@ -470,11 +482,11 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             const uint64_t need = (tiles + 3) / 4;
             if (mode == 3) {
                 auto kern = v1_fast_kernel<BatterySink, 0>;
-                const size_t sm = 4 * BatterySink::kSmemBytesPerWarp;
+                const size_t sm = 4 * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
             } else {
                 auto kern = v1_fast_kernel<StatsSink, 0>;
-                const size_t sm = 4 * StatsSink::kSmemBytesPerWarp;
+                const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
             }
         }
@@ -484,11 +496,11 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
         const uint64_t need = (tiles + wpb - 1) / wpb;
         if (mode == 2) {
             auto kern = v1_general_kernel<StatsSink>;
-            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+            const size_t sm = wpb * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, need)), dim3(32 * wpb), sm, st, a);
         } else if (mode == 3) {
             auto kern = v1_general_kernel<BatterySink>;
-            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+            const size_t sm = wpb * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, need)), dim3(32 * wpb), sm, st, a);
         } else {
             int grid = blocks_for(tiles, wpb, 0);

@@ -24,7 +24,7 @@
 namespace ciprng {
 
 struct Bbs8 {
-    uint32_t y[8], nM[8], mu[8];  // nM = 2^32 - M
+    uint32_t y[8], nM[8], mu[8], K[8], iF[8];  // nM = 2^32 - M; K, iF: fbarrett_sq (device.cuh)
 };
 
 // y << k on the ALU pipe (funnel shift with a zero low word): the heavy FMA
@@ -37,6 +37,17 @@ __device__ __forceinline__ uint32_t shl_alu(uint32_t y) {
     return r;
 }
 
+// (t >> 4) | (y << 28): one funnel shift (SHF) that pushes y's low nibble in
+// at the top of t.  Applied for j = 7, 6, ..., 0 it builds
+// y0:y1:...:y7 (most significant first), Alg. 5's t = (t << 4) | (y_j & 15)
+// chain for j = 0..7, in 8 ALU instructions instead of 7
+// shifts + 7 merges; the 8 shifts flush t's initial bits.
+__device__ __forceinline__ uint32_t push_nibble(uint32_t t, uint32_t y) {
+    uint32_t r;
+    asm("shf.r.clamp.b32 %0, %1, %2, 4;" : "=r"(r) : "r"(t), "r"(y));
+    return r;
+}
+
 // bmsk: the low `n` bits set (n in 0..3 here), one BMSK instruction
 __device__ __forceinline__ uint32_t low_mask(uint32_t n) {
     uint32_t m;
@@ -44,38 +55,56 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t n) {
     return m;
 }
 
-// One number's strategy word.  The eight 4-bit fields are
-// placed independently (y_j << (28 - 4j), the multiply on the FMA pipe) and
-// merged by a 3-level LOP3 tree -- (hi & mask) | (lo & ~mask) -- instead of
-// the serial t = (t << 4) | nibble chain: same word, depth 3 instead of 8.
-// Each term y_j << (28 - 4j) is zero below its field, so ~mask keeps only
-// the lower operand's fields.
+// One squaring of instance j: instances in kFMask take the quotient from the
+// FP32 pipe (fbarrett_sq), the others Barrett with IMAD.HI (barrett_sq).
+template <uint32_t kFMask, int j>
+__device__ __forceinline__ uint32_t sq(Bbs8 &b) {
+    if constexpr ((kFMask >> j) & 1u)
+        b.y[j] = fbarrett_sq(b.y[j], b.nM[j], b.K[j], b.iF[j]);
+    else
+        b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
+    return b.y[j];
+}
+
+// One number's strategy word.  kPack: nibbles pushed in by one
+// funnel shift each (push_nibble); otherwise the eight 4-bit fields are
+// placed independently (y_j << (28 - 4j)) and merged by a 3-level LOP3 tree
+// -- (hi & mask) | (lo & ~mask) -- same word, depth 3 instead of 8.
+template <uint32_t kFMask, bool kPack>
 __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
-    const uint32_t f0 = shl_alu<28>(b.y[0]), f1 = shl_alu<24>(b.y[1]), f2 = shl_alu<20>(b.y[2]);
-    const uint32_t f3 = shl_alu<16>(b.y[3]), f4 = shl_alu<12>(b.y[4]), f5 = shl_alu<8>(b.y[5]);
-    const uint32_t f6 = shl_alu<4>(b.y[6]), f7 = b.y[7];
-    const uint32_t p01 = (f0 & 0xF0000000u) | (f1 & ~0xF0000000u);
-    const uint32_t p23 = (f2 & 0xFFF00000u) | (f3 & ~0xFFF00000u);
-    const uint32_t p45 = (f4 & 0xFFFFF000u) | (f5 & ~0xFFFFF000u);
-    const uint32_t p67 = (f6 & 0xFFFFFFF0u) | (f7 & ~0xFFFFFFF0u);
-    const uint32_t p03 = (p01 & 0xFF000000u) | (p23 & ~0xFF000000u);
-    const uint32_t p47 = (p45 & 0xFFFFFF00u) | (p67 & ~0xFFFFFF00u);
-    uint32_t t = (p03 & 0xFFFF0000u) | (p47 & 0x0000FFFFu);
+    uint32_t t;
+    if constexpr (kPack) {
+        t = push_nibble(0u, sq<kFMask, 7>(b));
+        t = push_nibble(t, sq<kFMask, 6>(b));
+        t = push_nibble(t, sq<kFMask, 5>(b));
+        t = push_nibble(t, sq<kFMask, 4>(b));
+        t = push_nibble(t, sq<kFMask, 3>(b));
+        t = push_nibble(t, sq<kFMask, 2>(b));
+        t = push_nibble(t, sq<kFMask, 1>(b));
+        t = push_nibble(t, sq<kFMask, 0>(b));
+    } else {
+        sq<kFMask, 0>(b), sq<kFMask, 1>(b), sq<kFMask, 2>(b), sq<kFMask, 3>(b);
+        sq<kFMask, 4>(b), sq<kFMask, 5>(b), sq<kFMask, 6>(b), sq<kFMask, 7>(b);
+        const uint32_t f0 = shl_alu<28>(b.y[0]), f1 = shl_alu<24>(b.y[1]), f2 = shl_alu<20>(b.y[2]);
+        const uint32_t f3 = shl_alu<16>(b.y[3]), f4 = shl_alu<12>(b.y[4]), f5 = shl_alu<8>(b.y[5]);
+        const uint32_t f6 = shl_alu<4>(b.y[6]), f7 = b.y[7];
+        const uint32_t p01 = (f0 & 0xF0000000u) | (f1 & ~0xF0000000u);
+        const uint32_t p23 = (f2 & 0xFFF00000u) | (f3 & ~0xFFF00000u);
+        const uint32_t p45 = (f4 & 0xFFFFF000u) | (f5 & ~0xFFFFF000u);
+        const uint32_t p67 = (f6 & 0xFFFFFFF0u) | (f7 & ~0xFFFFFFF0u);
+        const uint32_t p03 = (p01 & 0xFF000000u) | (p23 & ~0xFF000000u);
+        const uint32_t p47 = (p45 & 0xFFFFFF00u) | (p67 & ~0xFFFFFF00u);
+        t = (p03 & 0xFFFF0000u) | (p47 & 0x0000FFFFu);
+    }
     // two variable shifts with fillers: t <<= sh; t |= bbs & array_shift[sh]
-    b.y[2] = barrett_sq(b.y[2], b.nM[2], b.mu[2]);
-    uint32_t sh = b.y[2] & 3u;
-    b.y[0] = barrett_sq(b.y[0], b.nM[0], b.mu[0]);
-    t = (t << sh) | (b.y[0] & low_mask(sh));
-    b.y[6] = barrett_sq(b.y[6], b.nM[6], b.mu[6]);
-    sh = b.y[6] & 3u;
-    b.y[1] = barrett_sq(b.y[1], b.nM[1], b.mu[1]);
-    t = (t << sh) | (b.y[1] & low_mask(sh));
+    uint32_t sh = sq<kFMask, 2>(b) & 3u;
+    t = (t << sh) | (sq<kFMask, 0>(b) & low_mask(sh));
+    sh = sq<kFMask, 6>(b) & 3u;
+    t = (t << sh) | (sq<kFMask, 1>(b) & low_mask(sh));
     return t;
 }
 
-template <class Sink>
+template <class Sink, uint32_t kFMask, bool kPack>
 __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
@@ -106,9 +135,11 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         uint32_t x = sio.ld(16, sl), tp = sio.ld(17, sl);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const uint4 e = __ldg(modtab + m[j]);  // {M, mu, 2^32 - M, 0}
+            const uint4 e = __ldg(modtab + 2 * m[j]);  // {invMf, mu, 2^32 - M, K} (api.cu)
+            b.iF[j] = e.x;
             b.mu[j] = e.y;
             b.nM[j] = e.z;
+            b.K[j] = e.w;
         }
         if (!valid) {
 #pragma unroll
@@ -119,7 +150,7 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
         const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
         sink.begin_row(0, row);
         auto round = [&]() -> uint32_t {
-            uint32_t t = v2_strategy(b);
+            uint32_t t = v2_strategy<kFMask, kPack>(b);
             t ^= __shfl_sync(kFull, tp, src1) ^ __shfl_sync(kFull, tp, src2);
             tp = t;
             x ^= t;
@@ -150,21 +181,65 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
     sink.finish(a);
 }
 
-int launch_v2(const GenArgs &a, int mode, cudaStream_t st) {
+// Exhaustive device-side check of both squarings (the FP32 rounding modes
+// of fbarrett_sq are hardware behaviour the host emulation only models):
+// one thread per (modulus, y < 2^16); y >= M threads idle.
+__global__ void modsq_check_kernel(const uint32_t *mod, uint32_t n_mod, unsigned long long *bad) {
+    const uint32_t e = blockIdx.y, y = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_mod) return;
+    const uint4 w = reinterpret_cast<const uint4 *>(mod)[2 * e];  // {invMf, mu, 2^32 - M, K}
+    const uint32_t M = mod[kModWords * e + 4];
+    if (y >= M) return;
+    const uint32_t ref = (y * y) % M;
+    const uint32_t nb = (barrett_sq(y, w.z, w.y) != ref) + (fbarrett_sq(y, w.z, w.w, w.x) != ref);
+    if (nb) atomicAdd(bad, (unsigned long long)nb);
+}
+
+int launch_modsq_check(const uint32_t *mod, uint32_t n_mod, unsigned long long *bad, cudaStream_t st) {
+    modsq_check_kernel<<<dim3(65536 / 256, n_mod), 256, 0, st>>>(mod, n_mod, bad);
+    return 1;
+}
+
+// Default squaring split and nibble packing, from B200 measurements
+// (profiles/experiments/s33_v2_kinds.json, C3, L2 flushed): funnel-shift
+// packing 2.79e11 numbers/s vs 2.59e11 for the LOP3 tree (-10 % issued
+// instructions); moving 1-12 of the 12 squarings per number to the FP32
+// quotient gives 2.79e11 down to 2.59e11 -- never faster: the freed heavy-pipe
+// cycles are paid back in issue slots (7 instructions per squaring, not 4),
+// so every squaring stays Barrett. `kind` (CIPRNG_V2_KIND,
+// read at prng_create) selects another store-mode instantiation for experiments.
+constexpr uint32_t kV2FMask = 0x00;
+constexpr bool kV2Pack = true;
+
+int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int kind) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
     const int wpb = 8;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
-        auto kern = v2_kernel<StatsSink>;
-        const size_t sm = wpb * StatsSink::kSmemBytesPerWarp;
+        auto kern = v2_kernel<StatsSink, kV2FMask, kV2Pack>;
+        const size_t sm = wpb * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else if (mode == 3) {
-        auto kern = v2_kernel<BatterySink>;
-        const size_t sm = wpb * BatterySink::kSmemBytesPerWarp;
+        auto kern = v2_kernel<BatterySink, kV2FMask, kV2Pack>;
+        const size_t sm = wpb * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else {
-        launch_k(v2_kernel<StoreSink>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
+        void (*kern)(GenArgs) = v2_kernel<StoreSink, kV2FMask, kV2Pack>;
+        switch (kind) {
+            case 0: kern = v2_kernel<StoreSink, 0x00, false>; break;
+            case 1: kern = v2_kernel<StoreSink, 0x00, true>; break;
+            case 2: kern = v2_kernel<StoreSink, 0x08, true>; break;   // 1 FP32-quotient squaring per number
+            case 3: kern = v2_kernel<StoreSink, 0x01, true>; break;   // 2
+            case 4: kern = v2_kernel<StoreSink, 0x09, true>; break;   // 3
+            case 5: kern = v2_kernel<StoreSink, 0x03, true>; break;   // 4
+            case 6: kern = v2_kernel<StoreSink, 0x0B, true>; break;   // 5
+            case 7: kern = v2_kernel<StoreSink, 0x18, true>; break;   // 2 (two single-squared)
+            case 8: kern = v2_kernel<StoreSink, 0x01, false>; break;  // 2, LOP3 tree
+            case 9: kern = v2_kernel<StoreSink, 0xFF, true>; break;   // 12
+            default: break;
+        }
+        launch_k(kern, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
     }
     return 1;
 }

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) init_kernel(InitArgs a) {
             for (int j = 0; j < 8; ++j) {
                 const uint64_t w = seed_word(a.seed, s, j);
                 const uint32_t mi = (uint32_t)(w >> 32) % a.n_mod;
-                const uint32_t M = a.mod[4 * mi];
+                const uint32_t M = a.mod[kModWords * mi + 4];
                 uint32_t rr = 2u + (uint32_t)w % (M - 3u);
                 while (gcd_u32(rr, M) != 1u || (rr * rr) % M <= 1u) rr = (rr == M - 2u) ? 2u : rr + 1u;
                 P[j * L + r] = (rr * rr) % M;

@@ -11,6 +11,9 @@ namespace ciprng {
 
 struct GenArgs;
 
+// Words per entry of the V2 modulus table (api.cu modulus_table()).
+constexpr int kModWords = 8;
+
 // L2 residency of the handle's state planes (set by api.cu around each
 // launch): the state is read and written once per call (48 B/stream for V1)
 // while the output streams past it, so it is marked persisting in L2 and the
@@ -74,7 +77,7 @@ struct InitArgs {
     uint64_t first_stream;
     int variant;
     int paper_defaults;
-    const uint32_t *mod;  // V2: [n_mod][4] = {M, mu, 2^32 - M, 0}
+    const uint32_t *mod;  // V2: [n_mod][kModWords] = {invMf, mu, 2^32 - M, K, M, 0, 0, 0} (api.cu)
     uint32_t n_mod;
 };
 
@@ -98,7 +101,8 @@ int launch_init(const InitArgs &a, cudaStream_t st);
 int launch_v0(const GenArgs &a, int mode, cudaStream_t st);
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               const V1Tuning &tune);
-int launch_v2(const GenArgs &a, int mode, cudaStream_t st);
+int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int kind = -1);
+int launch_modsq_check(const uint32_t *mod, uint32_t n_mod, unsigned long long *bad, cudaStream_t st);
 int launch_v3(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st);
 int launch_v4(const GenArgs &a, int mode, cudaStream_t st);
 int launch_cbg(bool encrypt, int chaotic, uint64_t n_msgs, uint64_t L, const uint64_t *a0, const uint64_t *a1,

@@ -46,6 +46,7 @@ struct StoreSink {
     __device__ __forceinline__ void end_rows(uint32_t) {}
     __device__ __forceinline__ void finish(const GenArgs &) {}
     static constexpr int kSmemBytesPerWarp = 0;
+    static constexpr int kSmemBytesExtra = 0;
     static constexpr bool kStats = false;
 };
 
@@ -101,6 +102,7 @@ __device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_
 
 struct StatsSink {
     uint32_t hist;       // shared address of this warp's 256 u32 bins
+    uint32_t junk;       // shared address of the CTA's discard bins (invalid lanes)
     uint32_t out32;      // outside pairs since the last end_rows (< 2^31, host-checked n)
     uint64_t outside;    // this lane's outside pairs
     uint64_t pairs;      // this lane's valid pairs
@@ -115,31 +117,37 @@ struct StatsSink {
         for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
         __syncthreads();
         hist = smem_u32(all) + 1024u * (threadIdx.x >> 5);
+        junk = smem_u32(all) + 1024u * (blockDim.x >> 5);  // kSmemBytesExtra, never read
     }
-    __device__ __forceinline__ void bin(uint32_t o) {
-        const uint32_t off = shr_fma<22>(o) & 0x3FCu;  // (o >> 24) * 4
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist + off) : "memory");
+    // Invalid lanes (rows past s_count in a partial tile) run the same
+    // instructions -- no branch around the consumer inside the round loop --
+    // with their bins redirected to the discard area and their outside count
+    // dropped by end_rows.  Bin address = base + (x >> 24) * 4: SHF + LEA.
+    __device__ __forceinline__ void bin(uint32_t base, uint32_t o) {
+        uint32_t addr;
+        asm("{\n\t.reg .u32 b;\n\tshr.u32 b, %1, 24;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
     }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool valid) {
-        if (!valid) return;
-        bin(o0);
-        bin(o1);
-        bin(o2);
-        bin(o3);
+        const uint32_t base = valid ? hist : junk;
+        bin(base, o0);
+        bin(base, o1);
+        bin(base, o2);
+        bin(base, o3);
         count_outside(out32, o0, o1);
         count_outside(out32, o2, o3);
     }
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
-        if (!valid) return;
-        bin(o);
+        bin(valid ? hist : junk, o);
         if (i & 1) count_outside(out32, pend[slot], o);
         else pend[slot] = o;
     }
-    // after the rounds of a tile: this lane owned `rows` valid streams
+    // after the rounds of a tile: this lane owned `rows` valid streams (0 for
+    // an invalid lane, whose outside count is discarded)
     __device__ __forceinline__ void end_rows(uint32_t rows) {
-        outside += out32;
+        outside += rows ? out32 : 0u;
         out32 = 0;
         pairs += (uint64_t)rows * (n >> 1);
         pending += kMaxRowsPerWarpTile * n;
@@ -171,6 +179,7 @@ struct StatsSink {
         }
     }
     static constexpr int kSmemBytesPerWarp = 1024;
+    static constexpr int kSmemBytesExtra = 1024;  // the discard bins
     static constexpr bool kStats = true;
 };
 
@@ -277,6 +286,7 @@ struct BatterySink {
         }
     }
     static constexpr int kSmemBytesPerWarp = 1024;
+    static constexpr int kSmemBytesExtra = 0;
     static constexpr bool kStats = true;
 };
 

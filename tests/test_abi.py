@@ -31,7 +31,8 @@ def test_strerror_covers_all_statuses():
 
 
 def test_barrett_modsq_exhaustive():
-    """Every modulus of the table, every y < M: barrett_sq == y*y % M."""
+    """Every modulus of the table, every y < M: barrett_sq and fbarrett_sq
+    (host emulation of the FP32-quotient form) == y*y % M."""
     bad = ctypes.c_uint64(123)
     assert P.lib().prng_selftest_modsq(ctypes.byref(bad)) == 0
     assert bad.value == 0
@@ -111,6 +112,6 @@ def test_python_binding_mirrors_abi_names():
     """The binding exposes every C-ABI entry point that takes work under its
     own name (marshalling only; no compute on import)."""
     compute = [s for s in P.declared_symbols() if s not in (
-        "prng_strerror", "prng_last_cuda_error", "prng_selftest_modsq", "prng_version")]
+        "prng_strerror", "prng_last_cuda_error", "prng_selftest_modsq", "prng_selftest_modsq_gpu", "prng_version")]
     missing = [s for s in compute if not callable(getattr(P, s, None))]
     assert not missing, missing

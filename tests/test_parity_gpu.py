@@ -127,6 +127,27 @@ def test_v2_custom_tables(C):
     _check(W.V2, SEEDS[1], 96 if C < 32 else 128, [5, 64, 3], comb_size=C, comb=comb)
 
 
+def test_modsq_exhaustive_on_device():
+    """Both division-free squarings (Barrett and the FP32-quotient form) run
+    by a kernel for every modulus and every y < M == y*y % M: the FP32
+    round-toward-zero steps are then the hardware's, not the host model's."""
+    import ctypes
+
+    bad = ctypes.c_uint64(123)
+    assert P.lib().prng_selftest_modsq_gpu(ctypes.byref(bad)) == 0
+    assert bad.value == 0
+
+
+@pytest.mark.parametrize("kind", list(range(10)))
+def test_v2_kernel_kinds(monkeypatch, kind):
+    """Every V2 store-kernel instantiation (squaring split between Barrett and
+    the FP32 quotient, nibble packing by funnel shift or LOP3 tree; DESIGN.md
+    s6) is bit-identical to the oracle, incl. the per-call selection and
+    rotation over several calls and a ragged n."""
+    monkeypatch.setenv("CIPRNG_V2_KIND", str(kind))
+    _check(W.V2, SEEDS[0], 1024 + 32, [64, 5, 1, 66])
+
+
 def test_v2_hand_trace_injected(golden):
     """The hand-traced C=1 trace (tests/golden) through the GPU via set_state."""
     e = golden["hand_traces"]["v2_c1_trace"]

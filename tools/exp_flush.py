@@ -26,7 +26,7 @@ def flush(mode, k):
     if mode in ("write", "write+read"):
         wbuf.fill_(k)
     if mode in ("write+read", "read"):
-        torch.sum(rbuf, dtype=torch.int64, out=acc)
+        acc.copy_(rbuf.sum(dtype=torch.int64))
 
 
 res = {}
