@@ -88,7 +88,8 @@ def ncu_inst_per_number():
     32 lanes / numbers in the profiled launch)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), key=os.path.getmtime)
+    # newest by name (r1a < ... < r1m < r2a): mtimes of a fresh checkout carry no order
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
     for f in reversed(files):
         with open(f) as fh:
             caps = json.load(fh).get("captures", {})
@@ -516,6 +517,55 @@ def run_ours(args):
     return 0
 
 
+def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
+    """C5 (BASELINE configs[4]) as a job over every rank: V1 consumer mode on
+    a global stream space of 2^20 streams per GPU (rank r owns the contiguous
+    range [r 2^20, (r+1) 2^20)), n = 1024 per call; each call is the fused
+    consume kernel followed by ONE all-reduce (NCCL under torchrun, SUM) of
+    the 258 u64 statistics -- the a7 row, the path's only collective.  Timed
+    per call with CUDA events around consume + all-reduce (L2 flushed before
+    each call), max over ranks; value = numbers consumed by all ranks / time.
+    Checked: the reduced counters hold exactly the job's pairs and numbers,
+    and pi-hat lies within 5 sigma of pi."""
+    import math
+
+    import torch.distributed as tdist
+
+    from paper_1112_5239_b200 import dist as D
+
+    ws = tdist.get_world_size() if tdist.is_available() and tdist.is_initialized() else 1
+    rk = tdist.get_rank() if ws > 1 else 0
+    S, n = 2**20, 1024
+    first, n_local = D.shard_range(S * ws, ws, rk)
+    g = P.ChaoticPRNG(W.SEEDS[0], S * ws, P.V1, shard=(first, n_local))
+    acc = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)
+
+    def step():
+        stats.zero_()
+        g.consume(n, stats)
+        D.allreduce_sum_(stats)
+        acc.add_(stats)
+
+    s = timed(step, calls)  # 3 warm-up + `calls` timed steps, all accumulated
+    t = torch.tensor([s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    s = float(t.item())
+    g.close()
+    st = P.as_u64(acc)
+    steps = calls + 3
+    pairs, inside = int(st[1]), int(st[0])
+    p = math.pi / 4
+    sigma = 4 * math.sqrt(p * (1 - p) / pairs)
+    return {"value": S * ws * n / s, "unit": UNIT, "ms_per_call": s * 1e3, "n_gpus": ws,
+            "global_streams": S * ws, "n": n, "collective": "all_reduce SUM of 258 u64 per call "
+            + ("(NCCL)" if ws > 1 else "(no-op at 1 GPU)"),
+            "pairs_exact": pairs == steps * S * ws * n // 2,
+            "hist_total_exact": int(st[2:].sum()) == steps * S * ws * n,
+            "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma}
+
+
 def measure_secondary(P, torch, dev, args):
     """Other rows of SURVEY s8(a) on this GPU (not the headline): V2 store
     (C3), V0 store and V1 fused consumer; numbers/s with CUDA events."""
@@ -538,6 +588,8 @@ def measure_secondary(P, torch, dev, args):
         torch.cuda.synchronize()
         return sum(a.elapsed_time(b) for a, b in ev) / 1e3 / steps
 
+    if args.c5_only:
+        return {"c5_consume_allreduce": measure_c5_sharded(P, torch, dev, timed)}
     S, n = W.CONFIGS["C3"]["n_streams"], W.CONFIGS["C3"]["n"]
     g = P.ChaoticPRNG(W.SEEDS[0], S, P.V2)
     out = torch.empty((S, n), dtype=torch.int32, device=dev)
@@ -570,6 +622,7 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: g.consume(n5, stats), 10)
     res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
     g.close()
+    res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
     from paper_1112_5239_b200 import battery as B
 
     g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
@@ -622,6 +675,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--c5-only", action="store_true", help="secondary rows: only the sharded C5 consume + all-reduce")
     ap.add_argument("--streams", type=int, default=0, help="experiment override of streams per GPU")
     ap.add_argument("--rounds", type=int, default=0, help="experiment override of numbers per stream")
     args = ap.parse_args()

@@ -126,7 +126,13 @@ struct StatsSink {
     __device__ __forceinline__ void bin(uint32_t base, uint32_t o) {
         uint32_t addr;
         asm("{\n\t.reg .u32 b;\n\tshr.u32 b, %1, 24;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
+#if defined(CIPRNG_EXP_NOHIST)  // experiment: consumer without the histogram
+        (void)addr;
+#elif defined(CIPRNG_EXP_HIST_LANE)  // experiment: conflict-free bins (bin = lane)
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + 4u * (threadIdx.x & 31u)) : "memory");
+#else
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+#endif
     }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,

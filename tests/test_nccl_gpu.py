@@ -58,3 +58,19 @@ def test_bench_multi_rank_path_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["global_streams"] == 2 * 65536 and d["value"] > 0
     assert d["scaling"] == "weak" and "cpu_baseline" not in d
+
+
+def test_bench_c5_consume_allreduce_two_ranks():
+    """bench.py's C5 row across ranks (consume + SUM all-reduce of the 258
+    statistics per call, max-over-ranks timing): two ranks sharing the one
+    GPU here over gloo.  The reduced counters cover the whole job exactly."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "4", "--warmup", "3", "--streams", "65536", "--c5-only", "--e2e-steps", "1"]
+    env = dict(os.environ, CIPRNG_BENCH_BACKEND="gloo")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    c5 = d["secondary"]["c5_consume_allreduce"]
+    assert c5["n_gpus"] == 2 and c5["global_streams"] == 2 * 2**20
+    assert c5["pairs_exact"] and c5["hist_total_exact"] and c5["pi_within_5_sigma"]
