@@ -267,19 +267,20 @@ class L2Flush:
     the flush buffer's own DIRTY lines in L2, whose write-back to HBM would
     then land inside the next timed call (measured: write-only flush 1.484e12
     vs write+read 1.51-1.53e12 numbers/s, tools/exp_flush.py,
-    profiles/experiments/s32_flush.json); the read pass writes them back
+    profiles/experiments/s32_flush*.json); the read pass (an int32 amax:
+    a pure read reduction, no dtype-cast copy) writes them back
     before the timer starts and leaves L2 full of clean, unrelated lines, so
     the timed call still finds its state planes in HBM."""
 
     def __init__(self, torch, dev):
         self.w = torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
         self.r = torch.ones(64 * 2**20, dtype=torch.int32, device=dev)
-        self.acc = torch.empty((), dtype=torch.int64, device=dev)
+        self.acc = torch.empty((), dtype=torch.int32, device=dev)
         self.torch = torch
 
     def __call__(self, k: int) -> None:
         self.w.fill_(k)
-        self.acc.copy_(self.r.sum(dtype=self.torch.int64))
+        self.acc.copy_(self.torch.amax(self.r))
 
 
 def run_ours(args):
