@@ -567,6 +567,64 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
             "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma}
 
 
+def measure_c4_sharded(P, torch, dev):
+    """C4 (BASELINE configs[3]) as a job over every rank: V1, 2^23 streams x
+    256 numbers x 466 calls = 1,000,727,379,968 numbers, the stream space
+    split over the ranks (dist.shard_range: rank r owns a contiguous range
+    of whole 32-stream groups) -- strong scaling, no collective on the data
+    path.  (1) Throughput: the rank's 466 calls back to back (each call's
+    output, 8 GiB / N, exceeds L2), CUDA events on the launching stream, max
+    over ranks; value = all numbers / that time.  (2) Verification (untimed):
+    a fresh handle regenerates the shard and digests every call on device
+    (prng_digest: position-aware, additive across shards); the 466 per-call
+    digests are SUM-all-reduced once, so the list -- and its sha256 -- is the
+    same at every GPU count."""
+    import hashlib
+
+    import torch.distributed as tdist
+
+    from paper_1112_5239_b200 import dist as D
+
+    ws = tdist.get_world_size() if tdist.is_available() and tdist.is_initialized() else 1
+    rk = tdist.get_rank() if ws > 1 else 0
+    c4 = W.CONFIGS["C4"]
+    S, n, calls = c4["n_streams"], c4["n"], c4["calls"]
+    first, n_local = D.shard_range(S, ws, rk)
+    out = torch.empty((n_local, n), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    g = P.ChaoticPRNG(W.SEEDS[0], S, P.V1, shard=(first, n_local))
+    for _ in range(3):  # warm-up on a separate handle (state advanced; not verified)
+        g.generate(n, out=out)
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    a_ev.record(stream)
+    for _ in range(calls):
+        g.generate(n, out=out)
+    b_ev.record(stream)
+    torch.cuda.synchronize()
+    g.close()
+    t = torch.tensor([a_ev.elapsed_time(b_ev) / 1e3], dtype=torch.float64, device=dev)
+    if ws > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    sec = float(t.item())
+    g = P.ChaoticPRNG(W.SEEDS[0], S, P.V1, shard=(first, n_local))
+    acc = torch.zeros(calls, dtype=torch.int64, device=dev)
+    for c in range(calls):
+        g.generate(n, out=out)
+        P.digest(out, first_stream=first, acc=acc[c:c + 1])
+    g.close()
+    D.allreduce_sum_(acc)
+    dl = P.as_u64(acc)
+    numbers = S * n * calls
+    return {"value": numbers / sec, "unit": UNIT, "seconds": sec, "n_gpus": ws, "numbers": numbers,
+            "streams": S, "n": n, "calls": calls, "scaling": "strong",
+            "per_gpu_value": numbers / sec / ws,
+            "digests_first3": [int(v) for v in dl[:3]],
+            "digest_list_sha256": hashlib.sha256(dl.tobytes()).hexdigest()}
+
+
 def measure_secondary(P, torch, dev, args):
     """Other rows of SURVEY s8(a) on this GPU (not the headline): V2 store
     (C3), V0 store and V1 fused consumer; numbers/s with CUDA events."""
@@ -591,6 +649,8 @@ def measure_secondary(P, torch, dev, args):
 
     if args.c5_only:
         return {"c5_consume_allreduce": measure_c5_sharded(P, torch, dev, timed)}
+    if args.c4_only:
+        return {"c4_sharded_1e12": measure_c4_sharded(P, torch, dev)}
     S, n = W.CONFIGS["C3"]["n_streams"], W.CONFIGS["C3"]["n"]
     g = P.ChaoticPRNG(W.SEEDS[0], S, P.V2)
     out = torch.empty((S, n), dtype=torch.int32, device=dev)
@@ -624,6 +684,7 @@ def measure_secondary(P, torch, dev, args):
     res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
     g.close()
     res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
+    res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
     from paper_1112_5239_b200 import battery as B
 
     g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
@@ -677,6 +738,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--c5-only", action="store_true", help="secondary rows: only the sharded C5 consume + all-reduce")
+    ap.add_argument("--c4-only", action="store_true", help="secondary rows: only the sharded C4 10^12-number job")
     ap.add_argument("--streams", type=int, default=0, help="experiment override of streams per GPU")
     ap.add_argument("--rounds", type=int, default=0, help="experiment override of numbers per stream")
     args = ap.parse_args()

@@ -256,6 +256,16 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
         int kmode = mode;
         const CUtensorMap *tm = nullptr;
         V1Tuning tune = h->v1tune;
+        // Box shape by n (profiles/experiments/s35_band_by_n.jsonl, 2^20
+        // streams, L2 flushed): 2-D 32-round boxes (128-byte row pieces 4n
+        // bytes apart) win at n = 128 (1.51e12 vs 1.30e12) but lose ground as
+        // the row stride grows (n = 1024: 1.33e12); 3-D band boxes of 64
+        // rounds x 64 rows, 2 warps per CTA, write 256-byte row pieces and
+        // stay at 1.51-1.64e12 for every n >= 192.
+        if (!tune.shape_set && n >= 192 && n % 32 == 0) {
+            tune.cols = 64;
+            tune.wpb = 2;
+        }
         if (tune.cols >= 64 && n % 32 != 0) tune.cols = 32;  // band boxes need whole 32-round bands
         if (mode == 0 && fast) {
             const bool tma_ok = a.vec && n < (1ull << 31) && s_count < (1ull << 31);
@@ -371,12 +381,16 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
     if (const char *v = std::getenv("CIPRNG_V1_COLS")) {
         int c = std::atoi(v);
         if (c == 8 || c == 16 || c == 32 || c == 64 || c == 128) h->v1tune.cols = c;
+        h->v1tune.shape_set = true;
     }
     if (const char *v = std::getenv("CIPRNG_V1_PERSIST")) h->v1tune.grid_mode = std::atoi(v);
     if (const char *v = std::getenv("CIPRNG_V1_WPB")) {
         int w = std::atoi(v);
         if (w >= 1 && w <= 8) h->v1tune.wpb = w;
+        h->v1tune.shape_set = true;
     }
+    for (const char *knob : {"CIPRNG_V1_PERSIST", "CIPRNG_V1_BUFS", "CIPRNG_V1_TPW", "CIPRNG_V1_GRID", "CIPRNG_V1_PF"})
+        if (const char *v = std::getenv(knob); v && v[0]) h->v1tune.shape_set = true;
     if (const char *v = std::getenv("CIPRNG_V2_KIND")) h->v2_kind = std::atoi(v);
     h->v1tune.l2_prefetch = env_on("CIPRNG_V1_PF", false);
     h->v1tune.smem_stg = env_on("CIPRNG_V1_SMEM_STG", false);

@@ -94,6 +94,7 @@ struct V1Tuning {
     bool l2_prefetch = false; // 2-D TMA kernel: bulk-prefetch the next wave's state into L2 (+0.3 % flushed, -1.3 % steady: off, s18)
     int grid_mode = 0;    // band kernels: 0 = one tile per warp, -1 = persistent at
                           // full occupancy, k > 0 = persistent with k CTAs per SM
+    bool shape_set = false;  // cols / wpb given by the environment: no per-n choice
 };
 
 // mode: 0 = store (direct), 1 = store (TMA tiles, V1 fast only), 2 = consume

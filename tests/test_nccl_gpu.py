@@ -74,3 +74,23 @@ def test_bench_c5_consume_allreduce_two_ranks():
     c5 = d["secondary"]["c5_consume_allreduce"]
     assert c5["n_gpus"] == 2 and c5["global_streams"] == 2 * 2**20
     assert c5["pairs_exact"] and c5["hist_total_exact"] and c5["pi_within_5_sigma"]
+
+
+def test_bench_c4_digests_identical_at_1_and_2_ranks():
+    """bench.py's C4 row (10^12 numbers, stream space split over the ranks):
+    the per-call digest list is the same whether one rank owns every stream
+    or two ranks (gloo, sharing the one GPU here) split them."""
+    base = [os.path.join(ROOT, "bench.py"), "--steps", "4", "--warmup", "3", "--streams", "65536", "--c4-only",
+            "--e2e-steps", "1", "--no-cpu-baseline"]
+    r1 = subprocess.run([sys.executable] + base, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r1.returncode == 0, r1.stderr[-3000:]
+    d1 = json.loads([ln for ln in r1.stdout.splitlines() if ln.startswith("{")][-1])["secondary"]["c4_sharded_1e12"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}"] + base + ["--gpus", "2"]
+    env = dict(os.environ, CIPRNG_BENCH_BACKEND="gloo")
+    r2 = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r2.returncode == 0, r2.stderr[-3000:]
+    d2 = json.loads([ln for ln in r2.stdout.splitlines() if ln.startswith("{")][-1])["secondary"]["c4_sharded_1e12"]
+    assert d1["n_gpus"] == 1 and d2["n_gpus"] == 2 and d1["numbers"] == d2["numbers"] == 1000727379968
+    assert d1["digest_list_sha256"] == d2["digest_list_sha256"]
+    assert d1["digests_first3"] == d2["digests_first3"]

@@ -52,6 +52,15 @@ def test_v1_custom_tables(C):
         _check(W.V1, SEEDS[0], S, [5, 128, 3], comb_size=C, comb=comb)
 
 
+@pytest.mark.parametrize("S", [96, 4096 + 32, 65536])
+def test_v1_default_shape_by_n(S):
+    """The default V1 store picks its box shape by n (2-D 32-round boxes for
+    n < 192, 3-D 64-round band boxes for n >= 192, n % 32 == 0; api.cu):
+    calls alternating between the two shapes, incl. a partial last band
+    (n = 224), continue every stream bit-exactly."""
+    _check(W.V1, SEEDS[1], S, [192, 128, 256, 224, 1024, 36, 320], store_path=P.STORE_TMA)
+
+
 def test_v1_spec_tiny_tables():
     """T=4, c=2, comb1=[0,1], comb2=[1,0]."""
     _check(W.V1, 12345, 4, [1, 2, 7], comb_size=2, comb=np.array([0, 1, 1, 0], np.uint8))
