@@ -208,14 +208,23 @@ __global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_
                 }
             }
         } else {
-            for (; i + 4 <= a.n; i += 4) {
+            auto block4 = [&](uint64_t i4) {
                 uint32_t oA0, oA1, oA2, oA3, oB0, oB1, oB2, oB3;
                 round2(oA0, oB0);
                 round2(oA1, oB1);
                 round2(oA2, oB2);
                 round2(oA3, oB3);
-                sink.put4(0, i, oA0, oA1, oA2, oA3, valid);
-                sink.put4(1, i, oB0, oB1, oB2, oB3, valid);
+                sink.put4(0, i4, oA0, oA1, oA2, oA3, valid);
+                sink.put4(1, i4, oB0, oB1, oB2, oB3, valid);
+            };
+            if constexpr (Sink::kStats) {
+                // consumers: n < 2^24 (host-checked), 32-bit trip counter and
+                // index, as in the V1 consumer (gen_v1.cu)
+                const uint32_t n4 = (uint32_t)a.n & ~3u;
+                for (uint32_t i32 = 0; i32 != n4; i32 += 4) block4(i32);
+                i = n4;
+            } else {
+                for (; i + 4 <= a.n; i += 4) block4(i);
             }
             for (; i < a.n; ++i) {
                 uint32_t oA, oB;

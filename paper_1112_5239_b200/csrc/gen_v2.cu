@@ -157,9 +157,19 @@ __global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
             return x;
         };
         uint64_t i = 0;
-        for (; i + 4 <= a.n; i += 4) {
-            uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
-            sink.put4(0, i, o0, o1, o2, o3, valid);
+        if constexpr (Sink::kStats) {
+            // consumers: n < 2^24 (host-checked), 32-bit trip counter and index
+            const uint32_t n4 = (uint32_t)a.n & ~3u;
+            for (uint32_t i32 = 0; i32 != n4; i32 += 4) {
+                uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
+                sink.put4(0, i32, o0, o1, o2, o3, valid);
+            }
+            i = n4;
+        } else {
+            for (; i + 4 <= a.n; i += 4) {
+                uint32_t o0 = round(), o1 = round(), o2 = round(), o3 = round();
+                sink.put4(0, i, o0, o1, o2, o3, valid);
+            }
         }
         for (; i < a.n; ++i) sink.put1(0, i, round(), valid);
         sink.end_rows(valid ? 1u : 0u);
