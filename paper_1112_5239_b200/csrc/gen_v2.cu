@@ -104,8 +104,16 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
     return t;
 }
 
+// experiment-only occupancy / CTA-shape knobs (CIPRNG_NVCC_EXTRA), never set by build()
+#ifndef CIPRNG_V2_MINB
+#define CIPRNG_V2_MINB 1
+#endif
+#ifndef CIPRNG_V2_WPB
+#define CIPRNG_V2_WPB 8
+#endif
+
 template <class Sink, uint32_t kFMask, bool kPack>
-__global__ void __launch_bounds__(256) v2_kernel(GenArgs a) {
+__global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, CIPRNG_V2_MINB) v2_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
@@ -224,7 +232,7 @@ constexpr bool kV2Pack = true;
 int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int kind) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
-    const int wpb = 8;
+    const int wpb = CIPRNG_V2_WPB;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         auto kern = v2_kernel<StatsSink, kV2FMask, kV2Pack>;
