@@ -104,12 +104,15 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
     return t;
 }
 
-// experiment-only occupancy / CTA-shape knobs (CIPRNG_NVCC_EXTRA), never set by build()
+// occupancy / CTA-shape knobs (experiments set them through CIPRNG_NVCC_EXTRA).
+// Forcing 5 or 6 CTAs per SM (48 / 40 registers) spills and loses 5-8 %
+// (profiles/experiments/s36_v2_occupancy.txt): V2 is heavy-FMA-pipe bound,
+// not latency bound, at 32 resident warps per SM (64 registers).
 #ifndef CIPRNG_V2_MINB
 #define CIPRNG_V2_MINB 1
 #endif
 #ifndef CIPRNG_V2_WPB
-#define CIPRNG_V2_WPB 8
+#define CIPRNG_V2_WPB 4  // 4 warps per CTA: 2.82e11 vs 2.80e11 at 8 (profiles/experiments/s36)
 #endif
 
 template <class Sink, uint32_t kFMask, bool kPack>
