@@ -49,9 +49,10 @@ struct DeviceGuard {
 // component: primes p = 3 (mod 4) in [128, 256] by a sieve, products p < q
 // ascending, each as one 32-byte entry (kModWords words)
 //   {invMf = bits of RZ(1/M) as float, mu = floor(2^32 / M), 2^32 - M,
-//    K = 0x4B000000 * M mod 2^32, M, 0, 0, 0}
+//    K = 0x4B000000 * M mod 2^32, M, Mp = -M^{-1} mod 2^32, R2 = 2^64 mod M, 0}
 // so one 128-bit load gives a BBS instance everything both squarings need
 // (barrett_sq: mu, 2^32 - M; fbarrett_sq: invMf, 2^32 - M, K; device.cuh);
+// the second 128-bit half serves the Montgomery alternative (mont_sq: M, Mp, R2);
 // the negated modulus is stored rather than derived so each squaring ends in
 // one IMAD + one VIADDMNMX.
 static uint32_t rz_recip_bits(uint32_t M) {
@@ -75,8 +76,11 @@ std::vector<uint32_t> modulus_table() {
     std::sort(Ms.begin(), Ms.end());
     std::vector<uint32_t> tab;
     for (uint32_t M : Ms) {
+        uint32_t inv = M;  // Newton: M*M = 1 (mod 8) for odd M; each step doubles the valid bits
+        for (int k = 0; k < 4; ++k) inv *= 2u - M * inv;
+        const uint32_t R2 = (uint32_t)((((unsigned __int128)1) << 64) % M);
         const uint32_t e[kModWords] = {rz_recip_bits(M), (uint32_t)((1ull << 32) / M), 0u - M,
-                                       0x4B000000u * M, M, 0u, 0u, 0u};
+                                       0x4B000000u * M, M, 0u - inv, R2, 0u};
         tab.insert(tab.end(), e, e + kModWords);
     }
     return tab;
@@ -685,11 +689,16 @@ int prng_selftest_modsq(uint64_t *mismatches) {
     uint64_t bad = 0;
     for (size_t k = 0; k + kModWords <= tab.size(); k += kModWords) {
         const uint32_t invMf = tab[k], mu = tab[k + 1], nM = tab[k + 2], K = tab[k + 3], M = tab[k + 4];
-        if (nM != 0u - M || K != 0x4B000000u * M) ++bad;
+        const uint32_t Mp = tab[k + 5], R2 = tab[k + 6];
+        if (nM != 0u - M || K != 0x4B000000u * M || M * Mp != 0xFFFFFFFFu) ++bad;
         for (uint32_t y = 0; y < M; ++y) {
             const uint32_t ref = (y * y) % M;
             if (barrett_sq(y, nM, mu) != ref) ++bad;
             if (fbarrett_sq(y, nM, K, invMf) != ref) ++bad;
+            uint32_t yh = mont_enter(y, M, Mp, R2);
+            if (yh != (uint32_t)(((uint64_t)y << 32) % M) || mont_sq(yh, M, Mp) != ref ||
+                yh != (uint32_t)(((uint64_t)ref << 32) % M))
+                ++bad;
         }
     }
     *mismatches = bad;

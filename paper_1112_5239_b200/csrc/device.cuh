@@ -87,6 +87,43 @@ __host__ __device__ __forceinline__ uint32_t barrett_sq(uint32_t y, uint32_t nM,
     return r2 < r ? r2 : r;
 }
 
+// Montgomery form (north_star's "Montgomery-style" squaring; SURVEY s8(d)
+// asks for the Barrett-vs-Montgomery comparison).  R = 2^32, Mp = -M^{-1}
+// mod 2^32.  For a single word T with T < M^2 (or T < M):
+//   m = T*Mp (mod 2^32);  T + m*M = 0 (mod 2^32), so lo(m*M) = 2^32 - T when
+//   T != 0 and REDC(T) = (T + m*M) / 2^32 = hi(m*M) + [T != 0];
+//   REDC(T) < (M^2 + 2^32*M) / 2^32 < M + 1, and REDC(T) = M would need
+//   M | T, which for T = yh^2 or T = y*R2 (yh, y < M = pq) means T = 0, and
+//   T = 0 gives 0: the result is canonical with no final subtraction.
+// Squaring in the Montgomery domain, yh = y*R mod M: yh' = REDC(yh^2); the
+// canonical y' (whose low bits Alg. 5 consumes) costs a second REDC(yh').
+// Heavy-pipe cost per squaring: 3 IMAD + 2 IMAD.HI = 14 cycles per warp vs
+// Barrett's 8 -- built as a measured alternative (CIPRNG_V2_KIND=10),
+// exhaustively checked like the others.
+__host__ __device__ __forceinline__ uint32_t mont_redc(uint32_t T, uint32_t M, uint32_t Mp) {
+    const uint32_t m = T * Mp;
+#ifdef __CUDA_ARCH__
+    // [T != 0] as min(T, 1), the addend of one IMAD.HI (written in PTX: from
+    // C++ the compiler evaluates both hi(m*M) and hi(m*M) + 1 and selects)
+    uint32_t r;
+    asm("{\n\t.reg .u32 c;\n\tmin.u32 c, %1, 1;\n\tmad.hi.u32 %0, %2, %3, c;\n\t}"
+        : "=r"(r)
+        : "r"(T), "r"(m), "r"(M));
+    return r;
+#else
+    return (uint32_t)(((uint64_t)m * M) >> 32) + (T < 1u ? T : 1u);
+#endif
+}
+// enter: y*R mod M = REDC(y * (R^2 mod M)) (y*R2 < M^2)
+__host__ __device__ __forceinline__ uint32_t mont_enter(uint32_t y, uint32_t M, uint32_t Mp, uint32_t R2) {
+    return mont_redc(y * R2, M, Mp);
+}
+// one BBS squaring in Montgomery form: yh <- REDC(yh^2); returns canonical y
+__host__ __device__ __forceinline__ uint32_t mont_sq(uint32_t &yh, uint32_t M, uint32_t Mp) {
+    yh = mont_redc(yh * yh, M, Mp);
+    return mont_redc(yh, M, Mp);
+}
+
 // The same squaring with the quotient taken from the FP32 pipe, which runs
 // beside the heavy FMA sub-pipe (IMAD + FFMA interleaved: 118 lane-ops/clk/SM,
 // profiles/r1e_pipe_microbench.json), so the half-rate IMAD.HI leaves the

@@ -25,6 +25,7 @@ namespace ciprng {
 
 struct Bbs8 {
     uint32_t y[8], nM[8], mu[8], K[8], iF[8];  // nM = 2^32 - M; K, iF: fbarrett_sq (device.cuh)
+    uint32_t yh[8];                            // Montgomery kinds: y*2^32 mod M; nM, mu hold M, Mp
 };
 
 // y << k on the ALU pipe (funnel shift with a zero low word): the heavy FMA
@@ -56,10 +57,14 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t n) {
 }
 
 // One squaring of instance j: instances in kFMask take the quotient from the
-// FP32 pipe (fbarrett_sq), the others Barrett with IMAD.HI (barrett_sq).
+// FP32 pipe (fbarrett_sq), the others Barrett with IMAD.HI (barrett_sq);
+// kFMask == kMontMask runs every instance in Montgomery form (mont_sq).
+constexpr uint32_t kMontMask = 0x100;
 template <uint32_t kFMask, int j>
 __device__ __forceinline__ uint32_t sq(Bbs8 &b) {
-    if constexpr ((kFMask >> j) & 1u)
+    if constexpr (kFMask == kMontMask)
+        b.y[j] = mont_sq(b.yh[j], b.nM[j], b.mu[j]);
+    else if constexpr ((kFMask >> j) & 1u)
         b.y[j] = fbarrett_sq(b.y[j], b.nM[j], b.K[j], b.iF[j]);
     else
         b.y[j] = barrett_sq(b.y[j], b.nM[j], b.mu[j]);
@@ -146,16 +151,27 @@ __global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, CIPRNG_V2_MINB) v2_kernel(
         uint32_t x = sio.ld(16, sl), tp = sio.ld(17, sl);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const uint4 e = __ldg(modtab + 2 * m[j]);  // {invMf, mu, 2^32 - M, K} (api.cu)
-            b.iF[j] = e.x;
-            b.mu[j] = e.y;
-            b.nM[j] = e.z;
-            b.K[j] = e.w;
+            if constexpr (kFMask == kMontMask) {
+                const uint4 e = __ldg(modtab + 2 * m[j] + 1);  // {M, Mp, R2, 0} (api.cu)
+                b.nM[j] = e.x;
+                b.mu[j] = e.y;
+                b.K[j] = e.z;
+            } else {
+                const uint4 e = __ldg(modtab + 2 * m[j]);  // {invMf, mu, 2^32 - M, K} (api.cu)
+                b.iF[j] = e.x;
+                b.mu[j] = e.y;
+                b.nM[j] = e.z;
+                b.K[j] = e.w;
+            }
         }
         if (!valid) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) b.y[j] = 2u;
             x = tp = 0;
+        }
+        if constexpr (kFMask == kMontMask) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b.yh[j] = mont_enter(b.y[j], b.nM[j], b.mu[j], b.K[j]);
         }
         const uint32_t src1 = gbase + a.comb.t[b.y[0] & 7u][off];
         const uint32_t src2 = gbase + a.comb.t[8u + (b.y[1] & 7u)][off];
@@ -212,7 +228,10 @@ __global__ void modsq_check_kernel(const uint32_t *mod, uint32_t n_mod, unsigned
     const uint32_t M = mod[kModWords * e + 4];
     if (y >= M) return;
     const uint32_t ref = (y * y) % M;
-    const uint32_t nb = (barrett_sq(y, w.z, w.y) != ref) + (fbarrett_sq(y, w.z, w.w, w.x) != ref);
+    const uint4 v = reinterpret_cast<const uint4 *>(mod)[2 * e + 1];  // {M, Mp, R2, 0}
+    uint32_t yh = mont_enter(y, v.x, v.y, v.z);
+    const uint32_t ym = mont_sq(yh, v.x, v.y);
+    const uint32_t nb = (barrett_sq(y, w.z, w.y) != ref) + (fbarrett_sq(y, w.z, w.w, w.x) != ref) + (ym != ref);
     if (nb) atomicAdd(bad, (unsigned long long)nb);
 }
 
@@ -258,6 +277,7 @@ int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int kind) {
             case 7: kern = v2_kernel<StoreSink, 0x18, true>; break;   // 2 (two single-squared)
             case 8: kern = v2_kernel<StoreSink, 0x01, false>; break;  // 2, LOP3 tree
             case 9: kern = v2_kernel<StoreSink, 0xFF, true>; break;   // 12
+            case 10: kern = v2_kernel<StoreSink, kMontMask, true>; break;  // all 12 in Montgomery form
             default: break;
         }
         launch_k(kern, dim3((int)blocks), dim3(32 * wpb), 0, st, a);

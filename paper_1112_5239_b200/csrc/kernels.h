@@ -77,7 +77,7 @@ struct InitArgs {
     uint64_t first_stream;
     int variant;
     int paper_defaults;
-    const uint32_t *mod;  // V2: [n_mod][kModWords] = {invMf, mu, 2^32 - M, K, M, 0, 0, 0} (api.cu)
+    const uint32_t *mod;  // V2: [n_mod][kModWords] = {invMf, mu, 2^32 - M, K, M, Mp, R2, 0} (api.cu)
     uint32_t n_mod;
 };
 

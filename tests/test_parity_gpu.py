@@ -137,9 +137,10 @@ def test_v2_custom_tables(C):
 
 
 def test_modsq_exhaustive_on_device():
-    """Both division-free squarings (Barrett and the FP32-quotient form) run
-    by a kernel for every modulus and every y < M == y*y % M: the FP32
-    round-toward-zero steps are then the hardware's, not the host model's."""
+    """All three division-free squarings (Barrett, the FP32-quotient form and
+    Montgomery REDC) run by a kernel for every modulus and every y < M ==
+    y*y % M: the FP32 round-toward-zero steps are then the hardware's, not
+    the host model's."""
     import ctypes
 
     bad = ctypes.c_uint64(123)
@@ -147,11 +148,11 @@ def test_modsq_exhaustive_on_device():
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("kind", list(range(10)))
+@pytest.mark.parametrize("kind", list(range(11)))
 def test_v2_kernel_kinds(monkeypatch, kind):
     """Every V2 store-kernel instantiation (squaring split between Barrett and
-    the FP32 quotient, nibble packing by funnel shift or LOP3 tree; DESIGN.md
-    s6) is bit-identical to the oracle, incl. the per-call selection and
+    the FP32 quotient or all in Montgomery form, nibble packing by funnel
+    shift or LOP3 tree) is bit-identical to the oracle, incl. the per-call selection and
     rotation over several calls and a ragged n."""
     monkeypatch.setenv("CIPRNG_V2_KIND", str(kind))
     _check(W.V2, SEEDS[0], 1024 + 32, [64, 5, 1, 66])

@@ -34,7 +34,7 @@ ms = sum(a.elapsed_time(b) for a, b in ev) / K
 print(json.dumps({"bit_exact": ok, "numbers_per_s": S * n / (ms / 1e3), "ms": ms}))
 '''.replace("ROOT", repr(ROOT))
 res = {}
-kinds = [int(k) for k in sys.argv[1:]] or list(range(10))
+kinds = [int(k) for k in sys.argv[1:]] or list(range(11))
 for rep in range(2):
     for kind in kinds:
         env = dict(os.environ, CIPRNG_V2_KIND=str(kind))
