@@ -503,6 +503,11 @@ def run_ours(args):
         ctx["consume_over_optimized_no_store"] = secondary["c5_v1_consume"]["value"] / 2.0e10
     if "c3_v2_store" in secondary:
         ctx["v2_store_over_bbs"] = secondary["c3_v2_store"]["value"] / 7.0e8
+    for key, row, ref in (("v3_consume_over_optimized_no_store", "c5_v3_consume", 2.0e10),
+                          ("v0_consume_over_naive_no_store", "c5_v0_consume", 2.75e9),
+                          ("v2_consume_over_bbs", "c5_v2_consume", 7.0e8)):
+        if row in secondary:
+            ctx[key] = secondary[row]["value"] / ref
     line["paper_context"] = ctx
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = time_oracle(args.cpu_seconds)
@@ -683,6 +688,16 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: g.consume(n5, stats), 10)
     res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
     g.close()
+    # the other variants in consumer mode (SURVEY s8(d) C5 "also V0 and V2"):
+    # the like-for-like rows for the paper's no-store figures -- V3 is its
+    # "optimized" xor64 kernel, V0 its naive Listing 1, V2 its BBS kernel
+    for name, var in (("c5_v0_consume", P.V0), ("c5_v2_consume", P.V2), ("c5_v3_consume", P.V3)):
+        g = P.ChaoticPRNG(W.SEEDS[0], S5, var)
+        st5 = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)
+        s = timed(lambda: g.consume(n5, st5), 10)
+        res[name] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5,
+                     "numbers_counted_exact": int(P.as_u64(st5)[2:].sum()) == 13 * S5 * n5}
+        g.close()
     res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
     res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
     from paper_1112_5239_b200 import battery as B
