@@ -416,7 +416,6 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         delete h;
         return PRNG_ENOMEM;
     }
-    h->evict_first = env_on("CIPRNG_EVICT_FIRST", true);
     {
         // evict-last only pays while the planes are a small part of L2 (V1 24
         // MiB, V3 16 MiB at 2^20 streams); for V0/V2/V4's 72-96 MiB it evicts
@@ -425,6 +424,11 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
         h->state_last = env_on("CIPRNG_STATE_EVICT_LAST", true) && l2 > 0 && words * 4 <= (size_t)l2 / 4;
     }
+    // Evict-first output stores pay only while they protect L2-resident state
+    // planes: with the planes kept (2^20 V1 streams) +2-5 %, with planes
+    // larger than the L2 budget (2^22-2^23 streams, C4 on one GPU) they cost
+    // 3-4 % (profiles/experiments/s38_evict_first_by_state.jsonl)
+    h->evict_first = env_on("CIPRNG_EVICT_FIRST", h->state_last);
     if (env_on("CIPRNG_L2PERSIST", false)) {
         // persisting-L2 carve-out (device-wide limit; only ever raised) sized
         // to the state planes, and a launch window covering them
