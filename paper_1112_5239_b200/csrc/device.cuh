@@ -319,12 +319,13 @@ struct GenArgs {
     uint64_t n;          // rounds per stream
     uint32_t *out;       // row 0 = stream s_begin; row stride n (store kernels)
     uint64_t *stats;     // consume kernels: 258 u64
-    const uint32_t *mod; // V2: [78][4] = {M, mu, 2^32 - M, 0}
+    const uint32_t *mod; // V2: [78][kModWords] = {invMf, mu, 2^32 - M, K, M, Mp, R2, 0} (api.cu)
     uint32_t C;          // combination_size
     uint32_t vec;        // 1: rows are 16-byte aligned, n % 4 == 0
     uint32_t evict_first; // 1: output stores carry an L2 evict-first hint
     uint32_t state_last;  // 1: state-plane loads/stores carry an L2 evict-last hint
     uint32_t pf_ahead;    // V1 TMA store: prefetch into L2 the state of tile + pf_ahead (0 = off)
+    uint32_t zero;        // always 0 (memset): a multiplier the compiler cannot fold (sinks.cuh)
     CombTables comb;
 };
 

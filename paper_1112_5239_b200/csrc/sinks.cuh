@@ -99,6 +99,27 @@ __device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_
         : "+r"(cnt)
         : "r"(u), "r"(v));
 }
+// The same with the counter's add-with-carry as zero*zero + cnt + CF
+// (madc: IMAD.X on the FMA pipe instead of IADD3.X on the ALU pipe; `zero`
+// is GenArgs::zero, a 0 the compiler cannot fold).  Experiment only
+// (CIPRNG_EXP_MADC): 4 fewer ALU instructions per 16 numbers, but measured
+// 3.7 % slower for V1 (1.61 vs 1.67e12), 1 % for V3
+// (profiles/experiments/s39_consume_madc.jsonl).
+__device__ __forceinline__ void count_outside_madc(uint32_t &cnt, uint32_t u, uint32_t v, uint32_t zero) {
+    asm("{\n\t"
+        ".reg .u64 U, V;\n\t"
+        ".reg .u32 ul, uh, vl, vh, d;\n\t"
+        "mul.wide.u32 U, %1, %1;\n\t"
+        "mul.wide.u32 V, %2, %2;\n\t"
+        "mov.b64 {ul, uh}, U;\n\t"
+        "mov.b64 {vl, vh}, V;\n\t"
+        "add.cc.u32 d, ul, vl;\n\t"
+        "addc.cc.u32 d, uh, vh;\n\t"
+        "madc.lo.u32 %0, %3, %3, %0;\n\t"
+        "}"
+        : "+r"(cnt)
+        : "r"(u), "r"(v), "r"(zero));
+}
 
 struct StatsSink {
     uint32_t hist;       // shared address of this warp's 256 u32 bins
@@ -110,8 +131,9 @@ struct StatsSink {
     uint64_t n;
     uint64_t pending;    // bin increments of this warp since its last flush (upper bound)
     uint64_t *gstats;
+    uint32_t zero;       // GenArgs::zero (count_outside_madc)
     __device__ __forceinline__ explicit StatsSink(const GenArgs &a)
-        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n), pending(0), gstats(a.stats) {
+        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n), pending(0), gstats(a.stats), zero(a.zero) {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
         for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
@@ -134,6 +156,13 @@ struct StatsSink {
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 #endif
     }
+    __device__ __forceinline__ void pair(uint32_t u, uint32_t v) {
+#if defined(CIPRNG_EXP_MADC)
+        count_outside_madc(out32, u, v, zero);
+#else
+        count_outside(out32, u, v);
+#endif
+    }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool valid) {
@@ -142,12 +171,12 @@ struct StatsSink {
         bin(base, o1);
         bin(base, o2);
         bin(base, o3);
-        count_outside(out32, o0, o1);
-        count_outside(out32, o2, o3);
+        pair(o0, o1);
+        pair(o2, o3);
     }
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
         bin(valid ? hist : junk, o);
-        if (i & 1) count_outside(out32, pend[slot], o);
+        if (i & 1) pair(pend[slot], o);
         else pend[slot] = o;
     }
     // after the rounds of a tile: this lane owned `rows` valid streams (0 for
