@@ -407,6 +407,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t.item())
     e2e_value = e2e_steps * S * n * ws / e2e_s
+    # the bound of the e2e path: a plain pinned device->host copy of the same
+    # bytes (torch, no generation) on this GPU's PCIe link
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        host.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h_gbs = e2e_steps * 4 * S * n / (time.perf_counter() - t0) / 1e9
 
     # ---- roofline of the dominant (only) kernel
     peak, peak_src, peaks = measured_peaks()
@@ -477,6 +485,9 @@ def run_ours(args):
             "d2h_bytes_per_step": 4 * S * n,
             "api": "prng_generate_host (pinned host buffer, chunked generate + D2H overlap)",
             "steps": e2e_steps,
+            "d2h_copy_gbs": d2h_gbs,
+            "frac_of_d2h_copy": e2e_value / ws * 4 / 1e9 / d2h_gbs,
+            "bound": "PCIe device->host: the e2e rate over a plain pinned copy of the same bytes",
         },
         "steady_state": {
             "value": steady_value,
