@@ -36,6 +36,12 @@ __all__ = ["ChaoticPRNG", "digest", "V0", "V1", "V2", "V3", "V4", "STATE_WORDS",
            "PrngError"]
 
 
+def _require(cond: bool, msg: str) -> None:
+    """Argument validation that survives ``python -O`` (unlike assert)."""
+    if not cond:
+        raise ValueError(msg)
+
+
 def _stream_handle(stream) -> ctypes.c_void_p:
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -80,7 +86,9 @@ class ChaoticPRNG:
         """One call of n rounds; returns int32 [n_local, n] (bit pattern = u32)."""
         if out is None:
             out = torch.empty((self.n_local, n), dtype=torch.int32, device=self.device)
-        assert out.is_cuda and out.is_contiguous() and out.numel() >= self.n_local * n and out.element_size() == 4
+        _require(out.is_cuda and out.device == self.device, f"out must live on {self.device}")
+        _require(out.is_contiguous() and out.element_size() == 4 and out.numel() >= self.n_local * n,
+                 f"out must be a contiguous 4-byte tensor of >= {self.n_local} x {n} elements")
         check(lib().prng_generate(self._h, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
               "prng_generate")
         return out
@@ -89,7 +97,9 @@ class ChaoticPRNG:
         """Same words into a (pinned) host tensor, overlapping D2H with generation."""
         if out is None:
             out = torch.empty((self.n_local, n), dtype=torch.int32, pin_memory=True)
-        assert not out.is_cuda and out.is_contiguous() and out.numel() >= self.n_local * n
+        _require(not out.is_cuda and out.is_contiguous() and out.element_size() == 4
+                 and out.numel() >= self.n_local * n,
+                 f"out must be a contiguous 4-byte host tensor of >= {self.n_local} x {n} elements")
         check(lib().prng_generate_host(self._h, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
               "prng_generate_host")
         return out
@@ -98,7 +108,9 @@ class ChaoticPRNG:
         """Fused consumer: adds {inside, pairs, hist[256]} into int64 [258] (u64 bits)."""
         if stats is None:
             stats = torch.zeros(N_STATS, dtype=torch.int64, device=self.device)
-        assert stats.is_cuda and stats.numel() == N_STATS and stats.dtype == torch.int64
+        _require(stats.is_cuda and stats.device == self.device and stats.numel() == N_STATS
+                 and stats.dtype == torch.int64 and stats.is_contiguous(),
+                 f"stats must be a contiguous int64 [{N_STATS}] tensor on {self.device}")
         check(lib().prng_consume(self._h, n, ctypes.c_void_p(stats.data_ptr()), _stream_handle(stream)),
               "prng_consume")
         return stats
@@ -108,7 +120,9 @@ class ChaoticPRNG:
         int64 [264] (u64 bits).  P-values: ``battery.pvalues``."""
         if stats is None:
             stats = torch.zeros(N_BATTERY, dtype=torch.int64, device=self.device)
-        assert stats.is_cuda and stats.numel() == N_BATTERY and stats.dtype == torch.int64
+        _require(stats.is_cuda and stats.device == self.device and stats.numel() == N_BATTERY
+                 and stats.dtype == torch.int64 and stats.is_contiguous(),
+                 f"stats must be a contiguous int64 [{N_BATTERY}] tensor on {self.device}")
         check(lib().prng_battery(self._h, n, ctypes.c_void_p(stats.data_ptr()), _stream_handle(stream)),
               "prng_battery")
         return stats
@@ -149,6 +163,8 @@ class ChaoticPRNG:
 
 def digest(out: torch.Tensor, first_stream: int = 0, acc: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Position-aware verification digest of a [n_local, n] output block (Q28)."""
+    _require(out.is_cuda and out.dim() == 2 and out.is_contiguous() and out.element_size() == 4,
+             "out must be a contiguous 2-D 4-byte CUDA tensor")
     n_local, n = out.shape
     if acc is None:
         acc = torch.zeros(1, dtype=torch.int64, device=out.device)

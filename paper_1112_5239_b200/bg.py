@@ -15,6 +15,14 @@ def _p(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _vec(t: torch.Tensor | None, B: int, dtype, dev, name: str) -> None:
+    """A per-message vector argument: contiguous, [B], of `dtype`, on `dev` (None allowed only for S0)."""
+    if t is None:
+        return
+    if not (t.is_cuda and t.device == dev and t.dtype == dtype and t.numel() == B and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous {dtype} [{B}] tensor on {dev}")
+
+
 def _stream(stream):
     return ctypes.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
 
@@ -23,7 +31,10 @@ def encrypt(chaotic: bool, N: torch.Tensor, r: torch.Tensor, m: torch.Tensor, S0
             stream=None):
     """N, r: int64 [B]; m: uint8 [B, L]; S0: int32 [B] or None -> (c uint8 [B, L], y int64 [B])."""
     B, L = m.shape
-    assert N.is_cuda and N.dtype == torch.int64 and N.numel() == B and r.numel() == B and m.dtype == torch.uint8
+    if not (m.is_cuda and m.dtype == torch.uint8):
+        raise ValueError("m must be a uint8 [B, L] CUDA tensor")
+    for t, dt, name in ((N, torch.int64, "N"), (r, torch.int64, "r"), (S0, torch.int32, "S0")):
+        _vec(t, B, dt, m.device, name)
     m = m.contiguous()
     c = torch.empty_like(m)
     y = torch.empty(B, dtype=torch.int64, device=m.device)
@@ -36,6 +47,10 @@ def decrypt(chaotic: bool, p: torch.Tensor, q: torch.Tensor, c: torch.Tensor, y:
             S0: torch.Tensor | None = None, stream=None):
     """-> (m uint8 [B, L], status int32 [B]: 0 ok, 1 invalid key / y)."""
     B, L = c.shape
+    if not (c.is_cuda and c.dtype == torch.uint8):
+        raise ValueError("c must be a uint8 [B, L] CUDA tensor")
+    for t, dt, name in ((p, torch.int64, "p"), (q, torch.int64, "q"), (y, torch.int64, "y"), (S0, torch.int32, "S0")):
+        _vec(t, B, dt, c.device, name)
     c = c.contiguous()
     m = torch.empty_like(c)
     status = torch.empty(B, dtype=torch.int32, device=c.device)

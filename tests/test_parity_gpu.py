@@ -90,6 +90,28 @@ def test_v1_misaligned_output_falls_back():
     assert ei.value.status == -4
 
 
+def test_binding_rejects_bad_buffers():
+    """The binding validates buffers with exceptions (not asserts, which
+    python -O strips): wrong dtype size, too small, host vs device, stats
+    shape; the handle's state is untouched by a rejected call."""
+    g = P.ChaoticPRNG(SEEDS[0], 64, W.V1)
+    before = g.get_state()
+    with pytest.raises(ValueError):
+        g.generate(8, out=torch.empty((64, 8), dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        g.generate(8, out=torch.empty((64, 7), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        g.generate(8, out=torch.empty((64, 8), dtype=torch.int32))
+    with pytest.raises(ValueError):
+        g.generate_host(8, out=torch.empty((64, 8), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        g.consume(8, torch.zeros(257, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        g.battery(8, torch.zeros(P.N_BATTERY, dtype=torch.int32, device="cuda"))
+    assert np.array_equal(g.get_state(), before)
+    g.close()
+
+
 def test_v1_generate_host_matches_device():
     g1 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
     g2 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
