@@ -304,9 +304,11 @@ CIPRNG_API const char *prng_last_cuda_error(void);
 
 /* Host-side exhaustive self-check of the kernels' division-free BBS squarings
  * (P:1209-1211 asks for 32-bit modulus arithmetic only): for every modulus
- * of the table and every y < M, compares Barrett (IMAD.HI quotient) and the
- * FP32-quotient form (host emulation of its round-toward-zero steps) with
- * y*y % M.  Writes the number of mismatches; runs on the CPU (no GPU). */
+ * of the table and every y < M, compares Barrett (IMAD.HI quotient), the
+ * FP32-quotient form (host emulation of its round-toward-zero steps) and the
+ * Montgomery form (entry y*2^32 mod M, one REDC squaring, canonical exit)
+ * with y*y % M, and checks the table's derived words (2^32 - M, K, -M^-1).
+ * Writes the number of mismatches; runs on the CPU (no GPU). */
 CIPRNG_API int prng_selftest_modsq(uint64_t *mismatches);
 
 /* The same exhaustive check executed by a kernel on the current device (the
