@@ -90,6 +90,36 @@ def test_v1_misaligned_output_falls_back():
     assert ei.value.status == -4
 
 
+@pytest.mark.parametrize("variant", [W.V0, W.V1, W.V2, W.V3, W.V4])
+def test_zero_rounds_is_a_noop(variant):
+    """n_per_stream == 0 is a no-op for every variant (include/ciprng.h): no
+    launch, state untouched -- for V2 in particular no per-call rotation
+    (reading Q19) -- so a 0-round call between two calls changes nothing;
+    consume(0) adds nothing."""
+    info = _check(variant, SEEDS[0], 96, [5, 0, 8])
+    g = P.ChaoticPRNG(SEEDS[0], 96, variant)
+    before = g.get_state()
+    stats = g.consume(0)
+    assert g.info().kernel_launches == 0
+    assert not P.as_u64(stats).any() and np.array_equal(g.get_state(), before)
+    g.close()
+    assert info is not None
+
+
+def test_size_overflow_rejected_before_launch():
+    """n * n_local * 4 beyond size_t is PRNG_ESIZE, returned before any launch
+    (the pointer is never dereferenced); the state is untouched."""
+    import ctypes
+
+    g = P.ChaoticPRNG(SEEDS[0], 64, W.V1)
+    before = g.get_state()
+    dummy = torch.empty(4, dtype=torch.int32, device="cuda")
+    st = P.lib().prng_generate(g._h, 2**62, ctypes.c_void_p(dummy.data_ptr()), ctypes.c_void_p(0))
+    assert st == P._lib.PRNG_ESIZE and g.info().kernel_launches == 0
+    assert np.array_equal(g.get_state(), before)
+    g.close()
+
+
 def test_binding_rejects_bad_buffers():
     """The binding validates buffers with exceptions (not asserts, which
     python -O strips): wrong dtype size, too small, host vs device, stats
