@@ -79,7 +79,9 @@ def ncu_traffic():
 ISSUE_PEAK_TLANE = 148 * 4 * 32 * 1.965e9 / 1e12
 # ncu capture kind (tools/prof_kernels.py) -> (secondary key, numbers per launch)
 NCU_KINDS = {"v2": ("c3_v2_store", 2**20 * 64), "v0": ("v0_store", 2**20 * 128), "v3": ("v3_store", 2**20 * 128),
-             "v4": ("v4_store", 2**20 * 128), "consume": ("c5_v1_consume", 2**20 * 1024)}
+             "v4": ("v4_store", 2**20 * 128), "consume": ("c5_v1_consume", 2**20 * 1024),
+             "consume_v0": ("c5_v0_consume", 2**20 * 1024), "consume_v2": ("c5_v2_consume", 2**20 * 1024),
+             "consume_v3": ("c5_v3_consume", 2**20 * 1024)}
 
 
 def ncu_inst_per_number():
@@ -708,6 +710,8 @@ def measure_secondary(P, torch, dev, args):
         s = timed(lambda: g.consume(n5, st5), 10)
         res[name] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5,
                      "numbers_counted_exact": int(P.as_u64(st5)[2:].sum()) == 13 * S5 * n5}
+        if var == P.V2:
+            res[name]["heavy_fma_roofline"] = {"peak_squarings_per_s": sq_peak, "frac": 12 * S5 * n5 / s / sq_peak}
         g.close()
     res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
     res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
