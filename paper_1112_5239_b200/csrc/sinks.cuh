@@ -147,7 +147,12 @@ struct StatsSink {
     // dropped by end_rows.  Bin address = base + (x >> 24) * 4: SHF + LEA.
     __device__ __forceinline__ void bin(uint32_t base, uint32_t o) {
         uint32_t addr;
+#if defined(CIPRNG_EXP_BIN_HI)  // experiment: x >> 24 as IMAD.HI (FMA pipe) instead of SHF (ALU):
+        // V1 -4 %, V3 -0.8 %, V0 +0.3 % (profiles/experiments/s40_consume_bin_hi.jsonl), off
+        asm("{\n\t.reg .u32 b;\n\tmul.hi.u32 b, %1, 256;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
+#else
         asm("{\n\t.reg .u32 b;\n\tshr.u32 b, %1, 24;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
+#endif
 #if defined(CIPRNG_EXP_NOHIST)  // experiment: consumer without the histogram
         (void)addr;
 #elif defined(CIPRNG_EXP_HIST_LANE)  // experiment: conflict-free bins (bin = lane)

@@ -15,7 +15,7 @@ S, n, K = 2**20, 1024, 20
 res = {"build": os.environ.get("CIPRNG_NVCC_EXTRA", "")}
 fl = L2Flush(torch, torch.device("cuda"))
 st = torch.cuda.current_stream()
-for var in (P.V1, P.V3, P.V2):
+for var in (P.V1, P.V3, P.V2, P.V0):
     nn = 64 if var == P.V2 else n
     g = P.ChaoticPRNG(1, S, var)
     stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
