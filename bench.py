@@ -99,7 +99,8 @@ def ncu_inst_per_number():
         for kind, (key, numbers) in NCU_KINDS.items():
             for c in caps.get(kind, []):
                 if c.get("warp_insts"):
-                    out[key] = (c["warp_insts"] * 32 / numbers, os.path.relpath(f, ROOT), c.get("kernel"))
+                    pipes = {k: c[k] for k in ("pipe_alu_cycles_pct", "pipe_fmaheavy_cycles_pct") if k in c}
+                    out[key] = (c["warp_insts"] * 32 / numbers, os.path.relpath(f, ROOT), c.get("kernel"), pipes)
                     break
         if out:
             return out
@@ -429,7 +430,7 @@ def run_ours(args):
     secondary = {}
     if not args.no_secondary:
         secondary = measure_secondary(P, torch, dev, args)
-        for key, (ipn, src, kern) in ncu_inst_per_number().items():
+        for key, (ipn, src, kern, pipes) in ncu_inst_per_number().items():
             if key in secondary:
                 ach = secondary[key]["value"] * ipn / 1e12
                 secondary[key]["roofline"] = {
@@ -437,6 +438,15 @@ def run_ours(args):
                     "frac": ach / ISSUE_PEAK_TLANE, "inst_per_number": ipn, "kernel": kern,
                     "source": f"{src} (smsp__inst_executed x 32 / numbers); peak = 148 SMs x 4 schedulers x 32 "
                               "lanes x 1.965 GHz (DESIGN.md s6)"}
+                if pipes:
+                    # the binding integer pipe's busy fraction in the same capture
+                    # (ncu sm__pipe_{alu,fmaheavy}_cycles_active): the issue fraction
+                    # above understates kernels bound by one pipe
+                    heavy = pipes.get("pipe_fmaheavy_cycles_pct", 0.0)
+                    alu = pipes.get("pipe_alu_cycles_pct", 0.0)
+                    secondary[key]["roofline"]["binding_pipe"] = {
+                        "pipe": "fmaheavy" if heavy > alu else "alu", "busy_frac": max(heavy, alu) / 100.0,
+                        "alu_busy_frac": alu / 100.0, "fmaheavy_busy_frac": heavy / 100.0}
 
     line = {
         "metric": METRIC,

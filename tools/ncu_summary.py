@@ -31,6 +31,8 @@ METRICS = [
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "pipe_alu_pct"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "pipe_fma_pct"),
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "pipe_lsu_pct"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "pipe_fmaheavy_cycles_pct"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "pipe_alu_cycles_pct"),
     ("smsp__inst_executed.sum", "warp_insts"),
     ("lts__t_sectors_srcunit_tex_op_write.sum", "l2_write_sectors"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall_long_sb"),
