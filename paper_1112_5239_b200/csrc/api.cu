@@ -295,7 +295,7 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
             const bool tma_ok = a.vec && n < (1ull << 31) && s_count < (1ull << 31);
             if (h->store_path == PRNG_STORE_TMA && reinterpret_cast<uintptr_t>(out) % 16 != 0) return PRNG_EALIGN;
             if (h->store_path != PRNG_STORE_DIRECT && tma_ok) {
-                tm = tensor_map(h, out, n, s_count, 32);
+                tm = tensor_map(h, out, n, s_count, CIPRNG_V3_COLS);
                 if (tm) {
                     kmode = 1;
                     path = PRNG_STORE_TMA;

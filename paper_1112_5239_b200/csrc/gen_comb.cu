@@ -274,7 +274,7 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             launch_k(kern, dim3(comb_blocks(tiles, wpb, 0)), dim3(32 * wpb), smem, st, a, *tmap);
         } else if (mode == 1) {
-            constexpr int kCols = 32, wpb = 2;  // V3: wpb 4 measured 1.5 % slower (profiles/experiments/s18)
+            constexpr int kCols = CIPRNG_V3_COLS, wpb = CIPRNG_V3_WPB;  // kernels.h (s18, s41)
             const size_t smem = (size_t)wpb * 2 * kCombTileRows * kCols * 4 + 1024;
             auto kern = comb_fast_kernel<Src, StoreSink, kCols>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -81,6 +81,18 @@ struct InitArgs {
     uint32_t n_mod;
 };
 
+// V3 TMA store kernel shape (experiment knobs through CIPRNG_NVCC_EXTRA):
+// box width in rounds (8, 16 or 32) and warps per CTA.  Measured (C2 shape,
+// L2 flushed, profiles/experiments/s41_v3_box_shape.jsonl): 32-round boxes,
+// 1 warp per CTA 1.236e12 numbers/s; 2 warps 1.219e12; 16-round boxes
+// 1.17-1.20e12; 8-round 1.11e12.
+#ifndef CIPRNG_V3_COLS
+#define CIPRNG_V3_COLS 32
+#endif
+#ifndef CIPRNG_V3_WPB
+#define CIPRNG_V3_WPB 1
+#endif
+
 // Tuning of the V1 fast store kernel (defaults chosen from B200 measurements,
 // overridable for experiments with CIPRNG_V1_COLS / _WPB / _GRID).
 struct V1Tuning {
