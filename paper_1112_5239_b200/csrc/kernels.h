@@ -59,13 +59,24 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 }
 
 // Blocks of `kern` that are resident at once on the device (occupancy x SMs):
-// the grid of the persistent consumer / battery kernels.  A fixed 8 CTAs/SM
-// overshoots when registers limit residency to 7 (the consumer), leaving a
-// second partial wave.
+// the unit of the consumer / battery grids (persistent_grid below; sized from
+// the occupancy API because registers limit the consumer to 7 CTAs/SM).
 int resident_blocks(const void *kern, int threads, size_t smem);
+// Grid of the consumer / battery kernels: k waves of resident CTAs (k = 0:
+// one tile per warp, no cap; CIPRNG_NVCC_EXTRA=-DCIPRNG_PGRID_WAVES=k for
+// experiments).  Measured (consumers, 2^20 streams, L2 flushed,
+// profiles/experiments/s42_consume_grid_waves.jsonl), k = 1 / 2 / 3 / 4 / 0:
+// V1 1.669 / 1.687 / 1.693 / 1.690 / 1.689e12, V3 1.104 / 1.153 / 1.153 /
+// 1.152 / 1.151e12, V2 2.61 / 2.70 / 2.70 / 2.68 / 2.67e11 numbers/s -- a
+// single persistent wave leaves SMs idle behind the slowest warps.
+#ifndef CIPRNG_PGRID_WAVES
+#define CIPRNG_PGRID_WAVES 3
+#endif
 template <typename... KArgs>
 inline int persistent_grid(void (*kern)(KArgs...), int threads, size_t smem, uint64_t blocks_needed) {
-    const int r = resident_blocks(reinterpret_cast<const void *>(kern), threads, smem);
+    const int r = CIPRNG_PGRID_WAVES == 0 ? 0x7FFFFFFF
+                                          : CIPRNG_PGRID_WAVES * resident_blocks(reinterpret_cast<const void *>(kern),
+                                                                                 threads, smem);
     const uint64_t b = blocks_needed < (uint64_t)r ? blocks_needed : (uint64_t)r;
     return (int)(b ? b : 1);
 }
