@@ -35,8 +35,32 @@ __device__ __forceinline__ uint32_t fold6(uint64_t t1, uint64_t t2, uint64_t t3)
 // than the ALU op it saves, so every funnel stays an SHF.
 constexpr int kFunnelDefault = 0;
 
+// CTA shape knobs (experiments through CIPRNG_NVCC_EXTRA): warps per CTA,
+// min CTAs per SM for the register budget, and shared-memory padding per
+// store CTA (limits residency, so the wave count of the grid can be chosen).
+// Measured (profiles/experiments/s43_v0_cta_shape.jsonl): 4 or 8 warps per
+// CTA and 5.5 vs 6.9 waves all within 1 % (4.56-4.57e11); padding to fewer
+// resident warps -1 %, forcing 44 warps/SM (40 registers, spills) -29 %.
+#ifndef CIPRNG_V0_WPB
+#define CIPRNG_V0_WPB 8
+#endif
+#ifndef CIPRNG_V0_MINB
+#define CIPRNG_V0_MINB 1
+#endif
+#ifndef CIPRNG_V0_PAD_SMEM
+#define CIPRNG_V0_PAD_SMEM 0
+#endif
+
+// (an explicit minimum of 1 CTA/SM relaxes ptxas' register budget: 81 instead
+// of 48 registers here -- so the bound is only given for a minimum above 1)
+#if CIPRNG_V0_MINB > 1
+#define CIPRNG_V0_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V0_WPB, CIPRNG_V0_MINB)
+#else
+#define CIPRNG_V0_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V0_WPB)
+#endif
+
 template <class Sink, bool kComb, int kFun = kFunnelDefault>
-__global__ void __launch_bounds__(256) v0_kernel(GenArgs a) {
+__global__ void CIPRNG_V0_LAUNCH_BOUNDS v0_kernel(GenArgs a) {
     constexpr int kFunnelXor64 = kFun & 7, kFunnelXor128 = (kFun >> 3) & 7, kFunnelXorwow = (kFun >> 6) & 7;
     Sink sink(a);
     pdl_launch_dependents();
@@ -148,7 +172,7 @@ template <bool kComb>
 static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st) {
     if (a.s_count == 0) return 0;
     const uint64_t tiles = (a.s_count + 31) / 32;
-    const int wpb = 8;
+    const int wpb = CIPRNG_V0_WPB;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
         auto kern = v0_kernel<StatsSink, kComb>;
@@ -159,7 +183,10 @@ static int launch_v0x(const GenArgs &a, int mode, cudaStream_t st) {
         const size_t sm = wpb * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);
     } else {
-        launch_k(v0_kernel<StoreSink, kComb>, dim3((int)blocks), dim3(32 * wpb), 0, st, a);
+        auto kern = v0_kernel<StoreSink, kComb>;
+        if (CIPRNG_V0_PAD_SMEM > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CIPRNG_V0_PAD_SMEM);
+        launch_k(kern, dim3((int)blocks), dim3(32 * wpb), (size_t)CIPRNG_V0_PAD_SMEM, st, a);
     }
     return 1;
 }

@@ -120,8 +120,17 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
 #define CIPRNG_V2_WPB 4  // 4 warps per CTA: 2.82e11 vs 2.80e11 at 8 (profiles/experiments/s36)
 #endif
 
+// An explicit minimum of 1 CTA per SM is NOT the same as none: it lets ptxas
+// spend registers freely (72 instead of 64 here, 93 in the consumer), so the
+// bound is only given when a minimum above 1 is asked for.
+#if CIPRNG_V2_MINB > 1
+#define CIPRNG_V2_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V2_WPB, CIPRNG_V2_MINB)
+#else
+#define CIPRNG_V2_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V2_WPB)
+#endif
+
 template <class Sink, uint32_t kFMask, bool kPack>
-__global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, CIPRNG_V2_MINB) v2_kernel(GenArgs a) {
+__global__ void CIPRNG_V2_LAUNCH_BOUNDS v2_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
