@@ -17,6 +17,8 @@
 // conditional subtraction; device.cuh).  The neighbour exchange is two
 // data-dependent SHFL.IDX per number.  12 squarings (~5 integer ops each)
 // per number: integer-issue bound.
+#include <type_traits>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -120,17 +122,19 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
 #define CIPRNG_V2_WPB 4  // 4 warps per CTA: 2.82e11 vs 2.80e11 at 8 (profiles/experiments/s36)
 #endif
 
-// An explicit minimum of 1 CTA per SM is NOT the same as none: it lets ptxas
-// spend registers freely (72 instead of 64 here, 93 in the consumer), so the
-// bound is only given when a minimum above 1 is asked for.
-#if CIPRNG_V2_MINB > 1
-#define CIPRNG_V2_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V2_WPB, CIPRNG_V2_MINB)
-#else
-#define CIPRNG_V2_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V2_WPB)
-#endif
+// An explicit minimum of 1 CTA per SM is NOT the same as none (0): it lets
+// ptxas spend registers freely -- 72 instead of 64 in the store kernel
+// (2.80 vs 2.82e11 numbers/s), but 93 instead of 72 in the consumer, which
+// is faster with them (2.99 vs 2.95e11; profiles/experiments/s43).  So the
+// consumer instantiation asks for 1 and the others for none, unless a larger
+// minimum is set for an experiment.
+template <class Sink>
+constexpr int v2_min_blocks() {
+    return CIPRNG_V2_MINB > 1 ? CIPRNG_V2_MINB : (std::is_same<Sink, StatsSink>::value ? 1 : 0);
+}
 
 template <class Sink, uint32_t kFMask, bool kPack>
-__global__ void CIPRNG_V2_LAUNCH_BOUNDS v2_kernel(GenArgs a) {
+__global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, v2_min_blocks<Sink>()) v2_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
