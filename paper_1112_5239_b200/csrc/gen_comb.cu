@@ -17,6 +17,8 @@
 //    128-bit STG or 64-stream x 32-round TMA tiles (2-D bulk tensor store).
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -104,8 +106,13 @@ __global__ void __launch_bounds__(256) comb_general_kernel(GenArgs a) {
 // ======================================================================== fast
 constexpr int kCombTileRows = 64;
 
+template <class Sink, int kCols, bool kStg>
+constexpr int comb_fast_min_blocks() {
+    return (kLbForceMin1 || (std::is_same<Sink, StoreSink>::value && kCols > 0 && !kStg)) ? 1 : 0;
+}
+
 template <class Src, class Sink, int kCols, bool kStg = false>
-__global__ void __launch_bounds__(256) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(256, (comb_fast_min_blocks<Sink, kCols, kStg>())) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int X = Src::kPlanes, TP = Src::kPlanes + 1;
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kCombTileRows * (kCols > 0 ? kCols : 4) * 4;

@@ -15,6 +15,7 @@
 // (P:971-974), the group's shared cells exchanged by two SHFL.IDX per number
 // (any C | 32 and any arrays; the draw, not the shuffle, is the cost here).
 #include <cstdlib>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.h"
@@ -51,16 +52,19 @@ constexpr int kFunnelDefault = 0;
 #define CIPRNG_V0_PAD_SMEM 0
 #endif
 
-// (an explicit minimum of 1 CTA/SM relaxes ptxas' register budget: 81 instead
-// of 48 registers here -- so the bound is only given for a minimum above 1)
-#if CIPRNG_V0_MINB > 1
-#define CIPRNG_V0_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V0_WPB, CIPRNG_V0_MINB)
-#else
-#define CIPRNG_V0_LAUNCH_BOUNDS __launch_bounds__(32 * CIPRNG_V0_WPB)
-#endif
+// Launch-bounds minimum (kernels.h kLbForceMin1): 1 = relaxed register
+// budget, 0 = ptxas' default (48 registers for the V0 store, 81 with 1).
+template <class Sink, bool kComb>
+constexpr int v0_min_blocks() {
+    return CIPRNG_V0_MINB > 1 ? CIPRNG_V0_MINB
+           : (kLbForceMin1 || (std::is_same<Sink, StatsSink>::value && !kComb) ||
+              (std::is_same<Sink, StoreSink>::value && kComb))
+               ? 1
+               : 0;
+}
 
 template <class Sink, bool kComb, int kFun = kFunnelDefault>
-__global__ void CIPRNG_V0_LAUNCH_BOUNDS v0_kernel(GenArgs a) {
+__global__ void __launch_bounds__(32 * CIPRNG_V0_WPB, (v0_min_blocks<Sink, kComb>())) v0_kernel(GenArgs a) {
     constexpr int kFunnelXor64 = kFun & 7, kFunnelXor128 = (kFun >> 3) & 7, kFunnelXorwow = (kFun >> 6) & 7;
     Sink sink(a);
     pdl_launch_dependents();

@@ -19,6 +19,8 @@
 //    3 LOP3 per 2 numbers on top of the xor128 steps.  Stores either direct
 //    (128-bit STG of 4-round buffers) or through a per-warp shared-memory
 //    tile written to HBM by a 2-D TMA bulk tensor store.
+#include <type_traits>
+
 #include "device.cuh"
 #include "kernels.h"
 #include "sinks.cuh"
@@ -97,8 +99,13 @@ constexpr int kFastTileRows = 64;
 // the TMA path, written back by the warp itself with coalesced 128-bit STG
 // (8 lanes per 128-byte row piece, 4 rows per instruction) instead of a TMA
 // bulk tensor store; kept for the three-way store-path comparison.
+template <class Sink, int kCols, bool kStg>
+constexpr int v1_fast_min_blocks() {
+    return (kLbForceMin1 || (std::is_same<Sink, StoreSink>::value && kCols > 0 && !kStg)) ? 1 : 0;
+}
+
 template <class Sink, int kCols, int kBufs = 2, bool kStg = false>
-__global__ void __launch_bounds__(256) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(256, (v1_fast_min_blocks<Sink, kCols, kStg>())) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);

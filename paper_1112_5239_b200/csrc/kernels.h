@@ -92,6 +92,19 @@ struct InitArgs {
     uint32_t n_mod;
 };
 
+// Minimum-CTAs-per-SM operand of the generator kernels' launch bounds: 1
+// (explicit) relaxes ptxas' register budget, 0 leaves its default.  Chosen
+// per instantiation from B200 measurements (profiles/experiments/s44_launch_bounds.jsonl,
+// both budgets measured for every kernel): 1 for the V1 and V3 TMA store
+// kernels (+0.3 %, +1.4 %), the V0 consumer (+1.8 %) and the V4 store
+// (+0.7 %); 0 for the V1 / V3 consumers (-1.1 %, -2.9 % with 1) and the V0
+// store (-2.5 %).  -DCIPRNG_EXP_LB_MIN1 forces 1 everywhere (experiments).
+#ifdef CIPRNG_EXP_LB_MIN1
+constexpr bool kLbForceMin1 = true;
+#else
+constexpr bool kLbForceMin1 = false;
+#endif
+
 // V3 TMA store kernel shape (experiment knobs through CIPRNG_NVCC_EXTRA):
 // box width in rounds (8, 16 or 32) and warps per CTA.  Measured (C2 shape,
 // L2 flushed, profiles/experiments/s41_v3_box_shape.jsonl): 32-round boxes,
