@@ -104,8 +104,28 @@ constexpr int v1_fast_min_blocks() {
     return (kLbForceMin1 || (std::is_same<Sink, StoreSink>::value && kCols > 0 && !kStg)) ? 1 : 0;
 }
 
+// experiment: launch bounds of the consumer instantiation (threads, min CTAs).
+// Measured (profiles/experiments/s45_v1_consumer_bounds.jsonl): the default
+// (256, 0) = 72 registers 1.69e12; (128, 8) = 64 registers, 8 CTAs/SM -5 %;
+// (128, 0) = 80 registers -1.2 %.
+#ifndef CIPRNG_EXP_V1C_THREADS
+#define CIPRNG_EXP_V1C_THREADS 256
+#endif
+#ifndef CIPRNG_EXP_V1C_MINB
+#define CIPRNG_EXP_V1C_MINB 0
+#endif
+template <class Sink>
+constexpr int v1_fast_max_threads() {
+    return std::is_same<Sink, StatsSink>::value ? CIPRNG_EXP_V1C_THREADS : 256;
+}
+template <class Sink, int kCols, bool kStg>
+constexpr int v1_fast_min_blocks_x() {
+    return std::is_same<Sink, StatsSink>::value && CIPRNG_EXP_V1C_MINB > 0 ? CIPRNG_EXP_V1C_MINB
+                                                                            : v1_fast_min_blocks<Sink, kCols, kStg>();
+}
+
 template <class Sink, int kCols, int kBufs = 2, bool kStg = false>
-__global__ void __launch_bounds__(256, (v1_fast_min_blocks<Sink, kCols, kStg>())) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_blocks_x<Sink, kCols, kStg>())) v1_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kFastTileRows * (kCols > 0 ? kCols : 4) * 4;
     Sink sink(a);
