@@ -329,7 +329,13 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
 // Persistent: each warp walks tiles tile, tile + W, ...; the state of its
 // next tile is prefetched into registers while the current one computes.
 template <int kBands, int kBufs>
-__global__ void __launch_bounds__(256) v1_band_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+// launch-bounds minimum 1 = relaxed register budget (64 instead of 58):
+// 2^20 x 256 1.562 -> 1.595e12, 2^20 x 1024 +0.5 %, 2^23 x 256 unchanged
+// (profiles/experiments/s46_band_launch_bounds.jsonl)
+#ifndef CIPRNG_EXP_BAND_MINB
+#define CIPRNG_EXP_BAND_MINB 1
+#endif
+__global__ void __launch_bounds__(256, CIPRNG_EXP_BAND_MINB) v1_band_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr uint32_t kBoxRounds = 32 * kBands;
     constexpr uint32_t kBoxBytes = 64 * kBoxRounds * 4;
     pdl_launch_dependents();
