@@ -136,7 +136,9 @@ __device__ void keystream_xor(const Mont64 &M, uint64_t x0, bool chaotic, uint32
     if (x_end) *x_end = x;
 }
 
-__global__ void __launch_bounds__(256) cbg_encrypt_kernel(int chaotic, uint64_t n_msgs, uint64_t L,
+// relaxed register budget (explicit minimum of 1 CTA/SM): +2 % encryption
+// throughput (profiles/experiments/s47_misc_launch_bounds.jsonl)
+__global__ void __launch_bounds__(256, 1) cbg_encrypt_kernel(int chaotic, uint64_t n_msgs, uint64_t L,
                                                           const uint64_t *Ns, const uint32_t *S0s,
                                                           const uint64_t *rs, const uint8_t *m, uint8_t *c,
                                                           uint64_t *y) {
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(256) cbg_encrypt_kernel(int chaotic, uint64_t 
     keystream_xor(M, x0, chaotic != 0, S0s ? S0s[k] : 0u, L, m + k * L, c + k * L, y + k);
 }
 
-__global__ void __launch_bounds__(256) cbg_decrypt_kernel(int chaotic, uint64_t n_msgs, uint64_t L,
+__global__ void __launch_bounds__(256, 1) cbg_decrypt_kernel(int chaotic, uint64_t n_msgs, uint64_t L,
                                                           const uint64_t *ps, const uint64_t *qs,
                                                           const uint32_t *S0s, const uint8_t *c,
                                                           const uint64_t *ys, uint8_t *m, uint32_t *status) {
