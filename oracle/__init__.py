@@ -56,6 +56,7 @@ def lib():
         L.orc_bbs_step.argtypes, L.orc_bbs_step.restype = [u32, u32], u32
         L.orc_state_size.argtypes, L.orc_state_size.restype = [i32], ctypes.c_size_t
         L.orc_grid_init.argtypes, L.orc_grid_init.restype = [i32, u64, u64, u64, i32, vp], i32
+        L.orc_init_from_words.argtypes, L.orc_init_from_words.restype = [i32, vp, vp], i32
         L.orc_grid_generate.argtypes = [i32, vp, u64, u32, vp, u64, vp]
         L.orc_grid_generate.restype = i32
         L.orc_stats_words.argtypes, L.orc_stats_words.restype = [vp, u64, u64, vp], i32
@@ -148,6 +149,18 @@ def init_states(variant: int, seed: int, first_stream: int, n_local: int,
     if rc != 0:
         raise OracleError(f"orc_grid_init rc={rc}")
     return st
+
+
+def init_from_words(variant: int, words) -> np.ndarray:
+    """One stream's state (STATE_WORDS[variant] uint32) from 16 injected seeder
+    words w[k] (test hook: the Q11/Q21 word -> state mapping alone)."""
+    w = np.zeros(16, dtype=np.uint64)
+    w[: len(words)] = [int(v) & (2**64 - 1) for v in words]
+    st = np.zeros((1, STATE_WORDS[variant]), dtype=np.uint32)
+    rc = lib().orc_init_from_words(variant, _ptr(w), _ptr(st))
+    if rc != 0:
+        raise OracleError(f"orc_init_from_words rc={rc}")
+    return st[0]
 
 
 def generate(variant: int, states: np.ndarray, n: int, comb_size: int = 32,

@@ -37,8 +37,17 @@
  *   orc_stats_words       brute-force recount on tiny inputs; pi estimate
  *   orc_digest_words      parity unpinned (a verification hash defined by
  *                         this build; only its arithmetic is checked)
- *   seeder/comb/modulus   parity unpinned by the paper: defined by this
- *   table choices         build (Q6, Q11, Q13); the modulus table is pinned
+ *   orc_v*_init_words     word -> state mapping checked field by field
+ *   (seeders)             against the published SplitMix64 generator (Q11);
+ *                         zero guards reached by injected words and tied to
+ *                         Marsaglia's published first outputs; V2 seeds
+ *                         recomputed from the words (Q21 incl. the
+ *                         rejection loop, reached by injection) and each
+ *                         y_j a quadratic residue mod both prime factors
+ *                         (Euler's criterion; BBS seeds are squares,
+ *                         P:1203-1206)
+ *   comb/modulus tables   the CHOICE of seeder and default arrays is this
+ *                         build's (Q6, Q11, Q13); the modulus table is pinned
  *                         to P:1212-1214's constraints (primes = 3 mod 4,
  *                         M < 2^16).
  */
@@ -155,13 +164,44 @@ typedef struct {
     uint32_t pad;   /* always 0                             */
 } orc_v0_state;
 
-/* Per-stream initial state (Q11, Q12).  paper_defaults reproduces Listing 1
- * (x = 123123123) with Marsaglia's published seeds. */
-void orc_v0_init_one(uint64_t seed, uint64_t s, int paper_defaults, orc_v0_state *st)
+/* The 16 seeder words of stream s: w[k] = W(seed, s, k) (Q11). */
+static void seed_words(uint64_t seed, uint64_t s, uint64_t w[16])
+{
+    uint32_t k;
+    for (k = 0; k < 16; k++) w[k] = orc_splitmix_word(seed, s, k);
+}
+
+/* Per-stream initial state from the stream's seeder words w[k] = W(s, k)
+ * (Q11, Q12): a = w0, b = w1..w4, c = w5..w9, d = w10, x = lo w11; an
+ * all-zero generator state (a fixed point of every xorshift) is replaced by
+ * Marsaglia's published seeds.  Split from orc_v0_init_one so that tests can
+ * inject words that reach the zero guards. */
+void orc_v0_init_words(const uint64_t w[16], orc_v0_state *st)
 {
     int k;
     memset(st, 0, sizeof(*st));
+    st->a = w[0];
+    if (st->a == 0) st->a = 88172645463325252ull;              /* zero is a fixed point */
+    for (k = 0; k < 4; k++) st->b[k] = w[1 + k];
+    if ((st->b[0] | st->b[1] | st->b[2] | st->b[3]) == 0) {
+        st->b[0] = 123456789u; st->b[1] = 362436069u; st->b[2] = 521288629u; st->b[3] = 88675123u;
+    }
+    for (k = 0; k < 5; k++) st->c[k] = w[5 + k];
+    if ((st->c[0] | st->c[1] | st->c[2] | st->c[3] | st->c[4]) == 0) {
+        st->c[0] = 123456789u; st->c[1] = 362436069u; st->c[2] = 521288629u; st->c[3] = 88675123u;
+        st->c[4] = 5783321u;
+    }
+    st->d = w[10];
+    st->x = lo32(w[11]);
+}
+
+/* paper_defaults reproduces Listing 1 (x = 123123123) with
+ * Marsaglia's published seeds. */
+void orc_v0_init_one(uint64_t seed, uint64_t s, int paper_defaults, orc_v0_state *st)
+{
+    uint64_t w[16];
     if (paper_defaults) {
+        memset(st, 0, sizeof(*st));
         st->a = 88172645463325252ull;
         st->b[0] = 123456789u; st->b[1] = 362436069u; st->b[2] = 521288629u; st->b[3] = 88675123u;
         st->c[0] = 123456789u; st->c[1] = 362436069u; st->c[2] = 521288629u; st->c[3] = 88675123u;
@@ -170,19 +210,8 @@ void orc_v0_init_one(uint64_t seed, uint64_t s, int paper_defaults, orc_v0_state
         st->x = 123123123u;
         return;
     }
-    st->a = orc_splitmix_word(seed, s, 0);
-    if (st->a == 0) st->a = 88172645463325252ull;              /* zero is a fixed point */
-    for (k = 0; k < 4; k++) st->b[k] = orc_splitmix_word(seed, s, 1 + k);
-    if ((st->b[0] | st->b[1] | st->b[2] | st->b[3]) == 0) {
-        st->b[0] = 123456789u; st->b[1] = 362436069u; st->b[2] = 521288629u; st->b[3] = 88675123u;
-    }
-    for (k = 0; k < 5; k++) st->c[k] = orc_splitmix_word(seed, s, 5 + k);
-    if ((st->c[0] | st->c[1] | st->c[2] | st->c[3] | st->c[4]) == 0) {
-        st->c[0] = 123456789u; st->c[1] = 362436069u; st->c[2] = 521288629u; st->c[3] = 88675123u;
-        st->c[4] = 5783321u;
-    }
-    st->d = orc_splitmix_word(seed, s, 10);
-    st->x = lo32(orc_splitmix_word(seed, s, 11));
+    seed_words(seed, s, w);
+    orc_v0_init_words(w, st);
 }
 
 /* One call of Listing 1: returns the new x. */
@@ -211,15 +240,24 @@ typedef struct {
     uint32_t tp;    /* this thread's shared cell: previous round's t (Q8) */
 } orc_v1_state;
 
-void orc_v1_init_one(uint64_t seed, uint64_t s, orc_v1_state *st)
+/* V1 state from the seeder words: xor128 (a,b,c,d) = lo w0..w3 (all zero ->
+ * Marsaglia's seeds), x = lo w4, tp = lo w5 (Q8, Q11). */
+void orc_v1_init_words(const uint64_t w[16], orc_v1_state *st)
 {
     int k;
-    for (k = 0; k < 4; k++) st->g[k] = lo32(orc_splitmix_word(seed, s, k));
+    for (k = 0; k < 4; k++) st->g[k] = lo32(w[k]);
     if ((st->g[0] | st->g[1] | st->g[2] | st->g[3]) == 0) {
         st->g[0] = 123456789u; st->g[1] = 362436069u; st->g[2] = 521288629u; st->g[3] = 88675123u;
     }
-    st->x = lo32(orc_splitmix_word(seed, s, 4));
-    st->tp = lo32(orc_splitmix_word(seed, s, 5));
+    st->x = lo32(w[4]);
+    st->tp = lo32(w[5]);
+}
+
+void orc_v1_init_one(uint64_t seed, uint64_t s, orc_v1_state *st)
+{
+    uint64_t w[16];
+    seed_words(seed, s, w);
+    orc_v1_init_words(w, st);
 }
 
 /* ======================================================================== */
@@ -284,22 +322,32 @@ static uint32_t gcd32(uint32_t a, uint32_t b)
 /* One BBS step x_{n+1} = x_n^2 mod M; x < M < 2^16 so x^2 < 2^32. */
 uint32_t orc_bbs_step(uint32_t y, uint32_t M) { return (y * y) % M; }
 
-/* Q21 seed: y = r^2 mod M with gcd(r, M) = 1 and y not in {0, 1}. */
-void orc_v2_init_one(uint64_t seed, uint64_t s, orc_v2_state *st)
+/* Q21 seed from the seeder words: instance j takes modulus index
+ * m_j = hi(w_j) mod 78 and r = 2 + lo(w_j) mod (M-3), stepped (wrapping to
+ * 2) until gcd(r, M) = 1 and r^2 mod M > 1; its state is the quadratic
+ * residue y_j = r^2 mod M (BBS seeds are squares; cf. the
+ * x_0 = r^2 mod N of P:1344).  x = lo w8, tp = lo w9. */
+void orc_v2_init_words(const uint64_t w[16], orc_v2_state *st)
 {
     int j;
     build_moduli();
     for (j = 0; j < 8; j++) {
-        uint64_t w = orc_splitmix_word(seed, s, (uint32_t)j);
-        uint32_t mi = hi32(w) % (uint32_t)orc_moduli_n;
+        uint32_t mi = hi32(w[j]) % (uint32_t)orc_moduli_n;
         uint32_t M = orc_moduli_tab[mi];
-        uint32_t r = 2u + lo32(w) % (M - 3u);
+        uint32_t r = 2u + lo32(w[j]) % (M - 3u);
         while (gcd32(r, M) != 1u || (r * r) % M <= 1u) r = (r == M - 2u) ? 2u : r + 1u;
         st->y[j] = (r * r) % M;
         st->m[j] = mi;
     }
-    st->x = lo32(orc_splitmix_word(seed, s, 8));
-    st->tp = lo32(orc_splitmix_word(seed, s, 9));
+    st->x = lo32(w[8]);
+    st->tp = lo32(w[9]);
+}
+
+void orc_v2_init_one(uint64_t seed, uint64_t s, orc_v2_state *st)
+{
+    uint64_t w[16];
+    seed_words(seed, s, w);
+    orc_v2_init_words(w, st);
 }
 
 /* ======================================================================== */
@@ -331,25 +379,39 @@ typedef struct {
 /* Seeds (Q11 extended): V3 a = W(s,0) (0 -> Marsaglia's 88172645463325252),
  * x = lo W(s,1), tp = lo W(s,2).  V4: the generator words exactly as V0
  * (W(s,0..10) with V0's zero guards), x = lo W(s,11), tp = lo W(s,12). */
-void orc_v3_init_one(uint64_t seed, uint64_t s, orc_v3_state *st)
+void orc_v3_init_words(const uint64_t w[16], orc_v3_state *st)
 {
-    st->a = orc_splitmix_word(seed, s, 0);
+    st->a = w[0];
     if (st->a == 0) st->a = 88172645463325252ull;
-    st->x = lo32(orc_splitmix_word(seed, s, 1));
-    st->tp = lo32(orc_splitmix_word(seed, s, 2));
+    st->x = lo32(w[1]);
+    st->tp = lo32(w[2]);
 }
 
-void orc_v4_init_one(uint64_t seed, uint64_t s, orc_v4_state *st)
+void orc_v3_init_one(uint64_t seed, uint64_t s, orc_v3_state *st)
+{
+    uint64_t w[16];
+    seed_words(seed, s, w);
+    orc_v3_init_words(w, st);
+}
+
+void orc_v4_init_words(const uint64_t w[16], orc_v4_state *st)
 {
     orc_v0_state g;
     int k;
-    orc_v0_init_one(seed, s, 0, &g);
+    orc_v0_init_words(w, &g);
     st->a = g.a;
     for (k = 0; k < 4; k++) st->b[k] = g.b[k];
     for (k = 0; k < 5; k++) st->c[k] = g.c[k];
     st->d = g.d;
-    st->x = lo32(orc_splitmix_word(seed, s, 11));
-    st->tp = lo32(orc_splitmix_word(seed, s, 12));
+    st->x = lo32(w[11]);
+    st->tp = lo32(w[12]);
+}
+
+void orc_v4_init_one(uint64_t seed, uint64_t s, orc_v4_state *st)
+{
+    uint64_t w[16];
+    seed_words(seed, s, w);
+    orc_v4_init_words(w, st);
 }
 
 /* The strategy draws ("t = xor-like()"). */
@@ -409,6 +471,20 @@ int orc_grid_init(int variant, uint64_t seed, uint64_t first_stream, uint64_t n_
         for (s = 0; s < n_local; s++) orc_v4_init_one(seed, first_stream + s, &st[s]);
         return ORC_OK;
     }
+    return ORC_EINVAL;
+}
+
+/* Test hook: one stream's state from 16 injected seeder words (the word ->
+ * state mapping of Q11/Q21 without the SplitMix64 step), so that pins can
+ * reach the zero guards and the Q21 rejection loop. */
+int orc_init_from_words(int variant, const uint64_t *w, void *state)
+{
+    if (!w || !state) return ORC_EINVAL;
+    if (variant == 0) { orc_v0_init_words(w, (orc_v0_state *)state); return ORC_OK; }
+    if (variant == 1) { orc_v1_init_words(w, (orc_v1_state *)state); return ORC_OK; }
+    if (variant == 2) { orc_v2_init_words(w, (orc_v2_state *)state); return ORC_OK; }
+    if (variant == 3) { orc_v3_init_words(w, (orc_v3_state *)state); return ORC_OK; }
+    if (variant == 4) { orc_v4_init_words(w, (orc_v4_state *)state); return ORC_OK; }
     return ORC_EINVAL;
 }
 

@@ -497,3 +497,163 @@ def test_survey_vectors(golden):
     assert O.xorwow_64_seq(e["seed"], e["d"], 2) == e["outputs"] == e["published_32bit_xorwow"][:2]
     st = O.init_states(O.V0, 0, 0, 1, paper_defaults=True)
     assert O.generate(O.V0, st, 4)[0].tolist() == g["listing1_paper_defaults_first4"]["outputs"]
+
+
+# ------------------------------------------------ seeders (Q11, Q12, Q21)
+# The word -> state mapping of every variant, pinned to the published
+# SplitMix64 sequence (test_splitmix_published) through O.splitmix_word, and
+# its zero guards / rejection loop reached by injecting words
+# (O.init_from_words, the oracle's test hook).  Marsaglia's seeds are the
+# literals of the published code (tests/golden/published_sequences.json).
+MARS128 = [123456789, 362436069, 521288629, 88675123]
+XOR64_SEED = 88172645463325252
+
+
+def _u64(lo, hi):
+    return int(lo) | (int(hi) << 32)
+
+
+def _v0_fields(row):
+    """orc_v0_state as u32 words: a, b[4], c[5], d (u64 lo/hi pairs), x, pad."""
+    r = [int(v) for v in row]
+    u = [_u64(r[2 * k], r[2 * k + 1]) for k in range(11)]
+    return {"a": u[0], "b": u[1:5], "c": u[5:10], "d": u[10], "x": r[22]}
+
+
+@pytest.mark.parametrize("seed", W.SEEDS)
+def test_v0_seeding_word_mapping(seed):
+    """Q11/Q12: a = W(s,0), b = W(s,1..4), c = W(s,5..9), d = W(s,10),
+    x = lo W(s,11) -- W read from the published SplitMix64 generator."""
+    st = O.init_states(O.V0, seed, 1000, 3)
+    for r, s in enumerate(range(1000, 1003)):
+        w = [O.splitmix_word(seed, s, k) for k in range(12)]
+        f = _v0_fields(st[r])
+        assert f["a"] == w[0] and f["b"] == w[1:5] and f["c"] == w[5:10] and f["d"] == w[10]
+        assert f["x"] == w[11] & M32 and int(st[r, 23]) == 0
+
+
+def test_splitmix_word_is_published_generator_output():
+    """W(seed, s, k) is output number 16s+k+1 of SplitMix64 run from `seed`:
+    iterate the published recurrence (state += golden gamma, then mix) in
+    Python big integers and read outputs 17..32 as stream 1's words."""
+    seed, state, outs = 0xDEADBEEF, 0xDEADBEEF, []
+    for _ in range(48):
+        state = (state + 0x9E3779B97F4A7C15) % 2**64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) % 2**64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) % 2**64
+        outs.append(z ^ (z >> 31))
+    for s in range(3):
+        assert [O.splitmix_word(seed, s, k) for k in range(16)] == outs[16 * s:16 * s + 16]
+
+
+def test_v0_zero_guards_injected():
+    """An all-zero xorshift state is a fixed point (every step maps 0 to 0),
+    so each generator whose seeder words are all zero restarts from
+    Marsaglia's published seeds; the guarded states then reproduce the
+    published first outputs.  Guards are per generator and only fire on an
+    all-zero state."""
+    f = _v0_fields(O.init_from_words(O.V0, [0] * 16))
+    assert f["a"] == XOR64_SEED and f["b"] == MARS128 and f["c"] == MARS128 + [5783321]
+    assert f["d"] == 0 and f["x"] == 0
+    assert O.xor64_seq(f["a"], 1) == [8748534153485358512]
+    # only the xor128 block zero: the others keep their words
+    w = [7] + [0, 0, 0, 0] + [1, 2, 3, 4, 5, 99, 0xABCDEF0123456789]
+    f = _v0_fields(O.init_from_words(O.V0, w))
+    assert f["a"] == 7 and f["b"] == MARS128 and f["c"] == [1, 2, 3, 4, 5] and f["d"] == 99
+    assert f["x"] == 0x23456789
+    # a single non-zero word (even only in the high half) is not guarded
+    w = [0, 0, 0, 0, 1 << 40, 0, 0, 0, 0, 1 << 63, 0, 0]
+    f = _v0_fields(O.init_from_words(O.V0, w))
+    assert f["a"] == XOR64_SEED and f["b"] == [0, 0, 0, 1 << 40] and f["c"] == [0, 0, 0, 0, 1 << 63]
+
+
+@pytest.mark.parametrize("seed", W.SEEDS)
+def test_v1_seeding_word_mapping(seed):
+    """Q8/Q11: xor128 (a,b,c,d) = lo W(s,0..3), x = lo W(s,4), tp = lo W(s,5)."""
+    st = O.init_states(O.V1, seed, 77, 3)
+    for r, s in enumerate(range(77, 80)):
+        assert [int(v) for v in st[r]] == [O.splitmix_word(seed, s, k) & M32 for k in range(6)]
+
+
+def test_v1_zero_guard_on_low_words():
+    """The xor128-32 state is the LOW halves of W(s,0..3): words whose low
+    halves are all zero (high halves not) give the all-zero 32-bit state and
+    must take Marsaglia's seeds -> first output 3701687786 (published)."""
+    st = O.init_from_words(O.V1, [1 << 32, 5 << 40, 0, 1 << 63, 0x1_0000_0011, 0x2_0000_0022])
+    assert [int(v) for v in st] == MARS128 + [0x11, 0x22]
+    assert O.xor128_32_seq(MARS128, 1) == [3701687786]
+    st = O.init_from_words(O.V1, [0, 0, 0, 9, 1, 2])
+    assert [int(v) for v in st] == [0, 0, 0, 9, 1, 2]
+
+
+def test_v3_v4_zero_guards_injected():
+    st = O.init_from_words(O.V3, [0, 0xAAAA_BBBB_CCCC_DDDD, 3])
+    assert _u64(st[0], st[1]) == XOR64_SEED and int(st[2]) == 0xCCCCDDDD and int(st[3]) == 3
+    v4 = O.init_from_words(O.V4, [0] * 11 + [5, 6])
+    v0 = O.init_from_words(O.V0, [0] * 11 + [5, 6])
+    assert np.array_equal(v4[:22], v0[:22]) and int(v4[22]) == 5 and int(v4[23]) == 6
+
+
+def _bbs_moduli_independent():
+    """Q13 re-derived here: products p < q of the primes = 3 (mod 4) in
+    [128, 256] (P:1212-1214), ascending."""
+    primes = [p for p in range(128, 257) if p % 4 == 3 and all(p % d for d in range(2, p))]
+    return sorted(p * q for i, p in enumerate(primes) for q in primes[i + 1:]), primes
+
+
+def _q21_seed(w, mods):
+    """Q21 written out: modulus index hi(w) mod 78, r = 2 + lo(w) mod (M-3),
+    stepped until gcd(r, M) = 1 and r^2 mod M > 1; state y = r^2 mod M."""
+    mi = (w >> 32) % len(mods)
+    M = mods[mi]
+    r = 2 + (w & M32) % (M - 3)
+    while math.gcd(r, M) != 1 or pow(r, 2, M) <= 1:
+        r = 2 if r == M - 2 else r + 1
+    return pow(r, 2, M), mi, r
+
+
+@pytest.mark.parametrize("seed", W.SEEDS)
+def test_v2_seeding_q21_and_quadratic_residues(seed):
+    """BBS seeds are squares: x_{n+1} = x_n^2 mod M and the
+    Blum-Goldwasser recall starts from x_0 = r^2 mod N.  Each y_j is
+    the Q21 square of W(s, j)'s r, and -- Euler's criterion -- a quadratic
+    residue modulo BOTH prime factors of its modulus (an oracle that stored r
+    instead of r^2 would fail this for ~3/4 of the instances).  x = lo W(s,8),
+    tp = lo W(s,9)."""
+    mods, primes = _bbs_moduli_independent()
+    st = O.init_states(O.V2, seed, 4096, 64)
+    n_r_not_qr = 0
+    for row, s in zip(st, range(4096, 4160)):
+        for j in range(8):
+            y_exp, mi, r = _q21_seed(O.splitmix_word(seed, s, j), mods)
+            assert int(row[j]) == y_exp and int(row[8 + j]) == mi
+            M = mods[mi]
+            for p in (p for p in primes if M % p == 0):
+                assert pow(int(row[j]), (p - 1) // 2, p) == 1          # Euler: QR mod p
+                n_r_not_qr += pow(r, (p - 1) // 2, p) != 1
+        assert int(row[16]) == O.splitmix_word(seed, s, 8) & M32
+        assert int(row[17]) == O.splitmix_word(seed, s, 9) & M32
+    assert n_r_not_qr > 100        # the criterion does discriminate r from r^2
+
+
+def test_v2_seed_rejection_loop_injected():
+    """Q21's rejection steps, reached by injected words: r landing on a prime
+    factor of M (gcd != 1) and on a non-trivial square root of 1 (r^2 = 1
+    mod M, found by CRT) both step to the next admissible r (for the root r + 1 = 40 * 251 is
+    rejected too, so it steps twice)."""
+    mods, primes = _bbs_moduli_independent()
+    mi = 77
+    M = mods[mi]                       # 239 * 251 = 59989
+    p, q = 239, 251
+    assert p * q == M
+    # non-trivial root of 1: r = 1 (mod p), r = -1 (mod q)
+    root = next(r for r in range(2, M - 1) if r % p == 1 and r % q == q - 1)
+    assert pow(root, 2, M) == 1
+    assert root == 10039 and (root + 1) % q == 0   # so the root steps twice
+    for r0, r_expect in ((p, p + 1), (2 * q, 2 * q + 1), (root, root + 2)):
+        w = (mi << 32) | (r0 - 2)     # 2 + lo mod (M - 3) = r0
+        st = O.init_from_words(O.V2, [w] * 8 + [0, 0])
+        assert [int(v) for v in st[:8]] == [pow(r_expect, 2, M)] * 8
+        assert [int(v) for v in st[8:16]] == [mi] * 8
+        assert _q21_seed(w, mods)[2] == r_expect
