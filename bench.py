@@ -4,16 +4,20 @@
 Metric (BASELINE.json): 32-bit random numbers/s, whole job, and the fraction
 of the HBM write roofline.  One step = one prng_generate call of BASELINE
 configs[1] per GPU: V1 (Alg. 4, xor128 + neighbour combination), 2^20 streams
-x 128 numbers, stored to HBM (512 MiB per step); L2 is flushed (untimed)
-before every timed call so the 24 MiB of state start each call in HBM.  Multi-GPU (torchrun, one process per GPU): every rank owns 2^20
-consecutive streams of one global stream space (weak scaling); the store path
-has no collective at all.
+x 128 numbers, stored to HBM (512 MiB per step).  L2 is flushed between
+timed calls so the 24 MiB of state start each call in HBM, and each call is
+CHARGED the write-back of the output lines it left dirty in L2: a step's time
+is call + the following flush, minus the flush alone.
+Multi-GPU (one process per GPU): every rank owns 2^20 consecutive streams of
+one global stream space (weak scaling); the store path has no collective at
+all.  `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N processes.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 --impl reference times the CPU oracle (oracle/, plain single-threaded C) on
-this host on a bounded sample of the same workload: the paper ships no code,
-so the oracle is the reference arm.
+this host on the same C2 workload (every step a full 2^20 x 128 call): the
+paper ships no code, so the oracle is the reference arm.
 """
 from __future__ import annotations
 
@@ -27,6 +31,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
@@ -74,37 +80,68 @@ def ncu_traffic():
     return None
 
 
-# Integer-issue peak for the compute-bound rows: one warp
-# instruction per scheduler per clock = 148 SMs x 4 x 32 lanes x 1.965 GHz.
-ISSUE_PEAK_TLANE = 148 * 4 * 32 * 1.965e9 / 1e12
+# Issue peak (one warp instruction per scheduler per clock = 148 SMs x 4 x 32
+# lanes x 1.965 GHz) -- reported beside the pipe roofline of the
+# compute-bound rows, not as it.
+N_SM = 148
+SM_MAX_HZ = 1.965e9
+ISSUE_PEAK_TLANE = N_SM * 4 * 32 * SM_MAX_HZ / 1e12
 # ncu capture kind (tools/prof_kernels.py) -> (secondary key, numbers per launch)
 NCU_KINDS = {"v2": ("c3_v2_store", 2**20 * 64), "v0": ("v0_store", 2**20 * 128), "v3": ("v3_store", 2**20 * 128),
              "v4": ("v4_store", 2**20 * 128), "consume": ("c5_v1_consume", 2**20 * 1024),
              "consume_v0": ("c5_v0_consume", 2**20 * 1024), "consume_v2": ("c5_v2_consume", 2**20 * 1024),
-             "consume_v3": ("c5_v3_consume", 2**20 * 1024)}
+             "consume_v3": ("c5_v3_consume", 2**20 * 1024), "battery": ("v1_battery", 2**20 * 1024),
+             "cbg": ("cbg_encrypt", 2**18 * 1024)}
 
 
-def ncu_inst_per_number():
-    """lane instructions per number of each secondary kernel, from the newest
-    committed ncu capture (profiles/r*_ncu_summary.json: smsp__inst_executed x
-    32 lanes / numbers in the profiled launch)."""
+def ncu_captures():
+    """The newest committed ncu capture of each secondary kernel
+    (profiles/r*_ncu_summary.json, written by tools/ncu_summary.py from
+    `ncu --set full` reports): {secondary key: (capture, numbers per launch,
+    source file)}."""
     import glob
 
-    # newest by name (r1a < ... < r1m < r2a): mtimes of a fresh checkout carry no order
+    # newest by name (r1a < ... < r1zc < r2a): mtimes of a fresh checkout carry no order
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    out = {}
     for f in reversed(files):
         with open(f) as fh:
             caps = json.load(fh).get("captures", {})
-        out = {}
         for kind, (key, numbers) in NCU_KINDS.items():
+            if key in out:
+                continue
             for c in caps.get(kind, []):
-                if c.get("warp_insts"):
-                    pipes = {k: c[k] for k in ("pipe_alu_cycles_pct", "pipe_fmaheavy_cycles_pct") if k in c}
-                    out[key] = (c["warp_insts"] * 32 / numbers, os.path.relpath(f, ROOT), c.get("kernel"), pipes)
+                if c.get("warp_insts") and c.get("duration") and c.get("sm_clock"):
+                    out[key] = (c, numbers, os.path.relpath(f, ROOT))
                     break
-        if out:
-            return out
-    return {}
+    return out
+
+
+def pipe_roofline(rate: float, cap: dict, numbers: int, src: str) -> dict:
+    """Roofline of a compute-bound row against its BINDING integer pipe.
+
+    ncu gives, for one launch of `numbers` numbers, the busy fraction of the
+    ALU and heavy-FMA pipes (sm__pipe_{alu,fmaheavy}_cycles_active, % of peak
+    sustained over the elapsed cycles).  Busy pipe-cycles per number =
+    fraction x duration x SM clock x 148 SMs / numbers; `achieved` = that x
+    the live bench rate, `peak` = 148 SMs x the max SM clock (the pipe busy
+    every cycle on every SM), so `frac` is the live rate's busy fraction of
+    the binding pipe.  The issue-slot figure (instructions per number x rate
+    over the 4-scheduler issue peak) is reported beside it."""
+    alu = cap.get("pipe_alu_cycles_pct", 0.0) / 100.0
+    heavy = cap.get("pipe_fmaheavy_cycles_pct", 0.0) / 100.0
+    pipe, busy = ("fmaheavy", heavy) if heavy > alu else ("alu", alu)
+    cyc_per_number = busy * cap["duration"] * cap["sm_clock"] * N_SM / numbers
+    peak = N_SM * SM_MAX_HZ
+    ach = rate * cyc_per_number
+    ipn = cap["warp_insts"] * 32 / numbers
+    return {"bound": pipe, "achieved": ach / 1e12, "peak": peak / 1e12, "unit": "T pipe-cycles/s",
+            "frac": ach / peak, "pipe_cycles_per_number": cyc_per_number,
+            "ncu_busy_frac": {"alu": alu, "fmaheavy": heavy}, "kernel": cap.get("kernel"),
+            "source": f"{src} (ncu --set full: sm__pipe_*_cycles_active, gpu__time_duration, "
+                      "sm__cycles_elapsed.avg.per_second); peak = 148 SMs x 1.965 GHz",
+            "issue": {"inst_per_number": ipn, "achieved": rate * ipn / 1e12, "peak": ISSUE_PEAK_TLANE,
+                      "unit": "T lane-inst/s", "frac": rate * ipn / 1e12 / ISSUE_PEAK_TLANE}}
 
 
 class ClockSampler:
@@ -163,6 +200,20 @@ class ClockSampler:
         }
 
 
+def cpu_model() -> str | None:
+    """Host CPU model (/proc/cpuinfo), reported beside every CPU timing."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or None
+
+
 def time_oracle(seconds: float = 10.0, max_calls: int = 64):
     """The oracle as it stands, single thread, on the C2 workload (full 2^20
     streams x 128 per call), as many calls as fit in ~`seconds`."""
@@ -181,6 +232,7 @@ def time_oracle(seconds: float = 10.0, max_calls: int = 64):
         "value": numbers / el,
         "unit": UNIT,
         "cores": 1,
+        "cpu_model": cpu_model(),
         "kind": "oracle",
         "sample": f"{calls} call(s) of the full C2 workload (V1, 2^20 streams x 128) = {numbers} numbers, "
                   f"single-threaded C oracle, {el:.1f} s wall",
@@ -218,34 +270,37 @@ def time_oracle_all_cores(calls: int = 16):
     wall = time.perf_counter() - t0
     el = max(worker_s)
     numbers = calls * S_PER_GPU * N_PER_STREAM
-    return {"value": numbers / el, "unit": UNIT, "cores": P, "kind": "oracle",
+    return {"value": numbers / el, "unit": UNIT, "cores": P, "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"{calls} call(s) of the full C2 workload split over {P} processes (one per core) by "
                       f"32-stream groups; slowest worker {el:.1f} s ({wall:.1f} s wall incl. process start)"}
 
 
 # --------------------------------------------------------------------------
 def run_reference(args):
+    """The reference arm: the oracle as it stands, single-threaded on this
+    host's cores, on the SAME workload as our arm -- every step one full C2
+    call (V1, 2^20 streams x 128 numbers, state carried across steps).  Under
+    torchrun only rank 0 runs; the others exit 0 without work."""
     rank, ws, _ = env_rank()
     if rank != 0:
         return 0
     import oracle as O
 
-    # bounded sample per step: 2^15 streams x 128 of the C2 workload (~40 ms)
-    S_s = 2**15
-    st = O.init_states(W.V1, W.SEEDS[0], 0, S_s)
+    S, n = S_PER_GPU, N_PER_STREAM
+    st = O.init_states(W.V1, W.SEEDS[0], 0, S)
     for _ in range(args.warmup):
-        O.generate(W.V1, st, N_PER_STREAM)
+        O.generate(W.V1, st, n)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.generate(W.V1, st, N_PER_STREAM)
+        O.generate(W.V1, st, n)
     el = time.perf_counter() - t0
-    v = args.steps * S_s * N_PER_STREAM / el
+    v = args.steps * S * n / el
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": v,
         "unit": UNIT,
-        "n_gpus": ws,
+        "n_gpus": ws if ws > 1 else max(1, args.gpus),
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": el / args.steps * 1e3,
@@ -253,11 +308,13 @@ def run_reference(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u32",
-        "data": "synthetic (seeded)",
-        "config": {"workload": "C2 sample: V1 xor128 + neighbour combination, 2^15 streams x 128 numbers per step "
-                               "(bounded sample of 2^20 x 128)", "variant": "v1"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} steps x 2^15 streams x 128 numbers, single-threaded C oracle"},
+        "data": "synthetic (seeded; SplitMix64 per-stream seeding, seed 0x0123456789ABCDEF)",
+        "config": {"workload": "C2 (BASELINE configs[1]): V1 Alg.4 xor128 + neighbour combination (default C=32 "
+                               f"arrays), {S} streams x {n} numbers per step", "variant": "v1",
+                   "streams_per_gpu": S, "n_per_stream": n, "same_config_as_ours": True},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": f"{args.steps} steps x the full C2 call ({S} streams x {n} numbers), "
+                                   "single-threaded C oracle, rank 0 only"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -323,12 +380,18 @@ def run_ours(args):
     store_path_used = g.info().store_path
     torch.cuda.synchronize()
 
-    # (1) headline: L2 flushed between timed steps (L2Flush: 256 MiB write + read > the 126
-    # MB L2 before every call, outside the timed interval), each call timed
-    # with CUDA events on the launching stream -- the state planes (24 MiB)
-    # start every call in HBM.
+    # (1) headline: L2 flushed between timed steps (L2Flush: 256 MiB write +
+    # read > the 126 MB L2, so the 24 MiB of state planes start every call in
+    # HBM), each step timed with CUDA events on the launching stream.  A call
+    # ends with up to ~13 % of its output still dirty in L2; the flush after
+    # it pays that write-back.  So a step is timed as [call + the following
+    # flush] and CHARGED that span minus the mean time of a flush that
+    # follows a flush (clean L2): every byte the call writes reaches HBM
+    # inside its charged time.  The flush after step k is the pre-flush of
+    # step k+1.
     flush = L2Flush(torch, dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(lr) as clk:
         # the W warm-up steps again, flush included, right before the timed
         # region: after any idle gap (NVML start-up, the flush buffer's
@@ -337,20 +400,32 @@ def run_ours(args):
         for k in range(args.warmup):
             flush(k)
             g.generate(n, out=out)
+        flush(0)
         barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
-            flush(k)
             ev[k][0].record(stream)
             g.generate(n, out=out)
             ev[k][1].record(stream)
+            flush(k + 1)
+            ev[k][2].record(stream)
+        # the flush alone, after a flush (nothing of ours dirty in L2)
+        for k in range(args.steps):
+            flush(k)
+            fev[k][0].record(stream)
+            flush(k + 1)
+            fev[k][1].record(stream)
         torch.cuda.synchronize()
     barrier()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    event_ms = sum(a.elapsed_time(b) for a, b, _ in ev)
+    flush_alone_ms = sum(a.elapsed_time(b) for a, b in fev) / args.steps
+    charged_ms = sum(a.elapsed_time(c) for a, _, c in ev) - args.steps * flush_alone_ms
+    # never credit the call with a flush faster than the one that followed it
+    charged_ms = max(charged_ms, event_ms)
+    t = torch.tensor([charged_ms, event_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms, event_ms = float(t[0].item()), float(t[1].item())
     numbers = args.steps * S * n * ws
     value = numbers / (total_ms / 1e3)
     del flush
@@ -428,34 +503,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     d2h_gbs = e2e_steps * 4 * S * n / (time.perf_counter() - t0) / 1e9
 
-    # ---- roofline of the dominant (only) kernel
+    # ---- roofline of the dominant (only) kernel: SURVEY s8(d) counts 4 B
+    # written per number; the state (24 B read + 24 B written per stream per
+    # call) is reported beside it, not in `achieved`
     peak, peak_src, peaks = measured_peaks()
-    alg_bytes = 4 * S * n + 2 * STATE_BYTES_V1 * S
-    # every timed interval holds exactly one launch of this one kernel
-    avg_kern_s = total_ms / args.steps / 1e3
-    achieved = alg_bytes / avg_kern_s / 1e9
+    out_bytes = 4 * S * n
+    state_bytes = 2 * STATE_BYTES_V1 * S
+    avg_kern_s = total_ms / args.steps / 1e3       # charged time per launch (one launch per step)
+    achieved = out_bytes / avg_kern_s / 1e9
     traffic = ncu_traffic()
 
     secondary = {}
     if not args.no_secondary:
         secondary = measure_secondary(P, torch, dev, args)
-        for key, (ipn, src, kern, pipes) in ncu_inst_per_number().items():
+        for key, (cap, numbers_launch, src) in ncu_captures().items():
             if key in secondary:
-                ach = secondary[key]["value"] * ipn / 1e12
-                secondary[key]["roofline"] = {
-                    "bound": "alu", "achieved": ach, "peak": ISSUE_PEAK_TLANE, "unit": "T lane-inst/s",
-                    "frac": ach / ISSUE_PEAK_TLANE, "inst_per_number": ipn, "kernel": kern,
-                    "source": f"{src} (smsp__inst_executed x 32 / numbers); peak = 148 SMs x 4 schedulers x 32 "
-                              "lanes x 1.965 GHz (DESIGN.md s6)"}
-                if pipes:
-                    # the binding integer pipe's busy fraction in the same capture
-                    # (ncu sm__pipe_{alu,fmaheavy}_cycles_active): the issue fraction
-                    # above understates kernels bound by one pipe
-                    heavy = pipes.get("pipe_fmaheavy_cycles_pct", 0.0)
-                    alu = pipes.get("pipe_alu_cycles_pct", 0.0)
-                    secondary[key]["roofline"]["binding_pipe"] = {
-                        "pipe": "fmaheavy" if heavy > alu else "alu", "busy_frac": max(heavy, alu) / 100.0,
-                        "alu_busy_frac": alu / 100.0, "fmaheavy_busy_frac": heavy / 100.0}
+                secondary[key]["roofline"] = pipe_roofline(secondary[key]["value"], cap, numbers_launch, src)
 
     line = {
         "metric": METRIC,
@@ -479,7 +542,8 @@ def run_ours(args):
             "n_per_stream": n,
             "global_streams": S * ws,
             "store_path": {1: "direct", 2: "tma"}.get(store_path_used, str(store_path_used)),
-            "l2": "L2 flushed before every timed step (256 MiB write then 256 MiB read, untimed); output "
+            "l2": "L2 flushed between timed steps (256 MiB write then 256 MiB read); each step charged its "
+                  "deferred write-back (call + following flush - flush alone); output "
                   f"{4 * S * n >> 20} MiB per step per GPU, state {STATE_BYTES_V1 * S >> 20} MiB",
             "parallelism": f"stream-sharded x{ws} (no collective on the store path)",
         },
@@ -491,8 +555,16 @@ def run_ours(args):
             "frac": achieved / peak,
             "traffic": traffic,
             "kernel": "v1_fast_kernel<StoreSink>",
-            "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_per_launch": out_bytes,
+            "alg_bytes_rule": "4 B written per number (SURVEY s8(d) C2); state reported separately",
+            "state_bytes_per_launch": state_bytes,
+            "achieved_incl_state": (out_bytes + state_bytes) / avg_kern_s / 1e9,
             "avg_kernel_ms": avg_kern_s * 1e3,
+            "timing": "charged: per step (call + following L2 flush) - mean(flush after a flush); the call's "
+                      "deferred write-back of dirty output lines is inside its time",
+            "event_only_ms": event_ms / args.steps,
+            "deferred_writeback_ms": (total_ms - event_ms) / args.steps,
+            "flush_alone_ms": flush_alone_ms,
             "peak_source": peak_src,
             # the metric's "% of HBM write roofline" against a write-only stream
             # (a copy peak counts read + write turnarounds a writer does not pay)
@@ -514,7 +586,7 @@ def run_ours(args):
             "value": steady_value,
             "unit": UNIT,
             "ms_per_step": steady_ms / args.steps,
-            "frac": alg_bytes / (steady_ms / args.steps / 1e3) / 1e9 / peak,
+            "frac": out_bytes / (steady_ms / args.steps / 1e3) / 1e9 / peak,
             "note": "back-to-back calls, no L2 flush: output stored evict-first, so the 24 MiB of state "
                     "planes stay L2-resident across calls (only the output reaches HBM)",
             "cuda_graph_value": graph_value,
@@ -586,6 +658,14 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
         acc.add_(stats)
 
     s = timed(step, calls)  # 3 warm-up + `calls` timed steps, all accumulated
+    # verification (untimed): the fixed C5 stream space (2^23 streams, n =
+    # 1024, one call) consumed sharded over however many ranks run, counters
+    # SUM-all-reduced -- their sha256 is the same at every GPU count
+    import hashlib
+
+    c5 = W.CONFIGS["C5"]
+    vstats = D.sharded_consume(W.SEEDS[0], c5["n_streams"], P.V1, c5["n"], 1)
+    vsha = hashlib.sha256(P.as_u64(vstats).tobytes()).hexdigest()
     t = torch.tensor([s], dtype=torch.float64, device=dev)
     if ws > 1:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -601,7 +681,48 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
             + ("(NCCL)" if ws > 1 else "(no-op at 1 GPU)"),
             "pairs_exact": pairs == steps * S * ws * n // 2,
             "hist_total_exact": int(st[2:].sum()) == steps * S * ws * n,
-            "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma}
+            "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma,
+            "verify": {"streams": c5["n_streams"], "n": c5["n"], "calls": 1,
+                       "stats_sha256": vsha, "note": "fixed global stream space; identical at every GPU count"}}
+
+
+def measure_c1(P, torch, dev, with_oracle: bool) -> dict:
+    """C1 (BASELINE configs[0]): V0 with `paper_defaults` --
+    Listing 1 exactly (x = 123123123, Marsaglia's seeds) -- ONE
+    stream, 10^6 outputs in one call.  One GPU thread runs the 10^6 dependent
+    Listing-1 steps (a latency-bound parity config, no roofline).  The oracle
+    (single host core, same workload) is timed beside it and its words
+    compared with the GPU's; the paper ran Listing 1 at 138 MS/s on one Xeon
+    core (P:1040-1041)."""
+    n = 10**6
+    stream = torch.cuda.current_stream()
+    g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
+    out = torch.empty((1, n), dtype=torch.int32, device=dev)
+    g.generate(n, out=out)                       # call 1: the parity call
+    first = P.as_u32(out.cpu()).copy()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    a.record(stream)
+    for _ in range(reps):
+        g.generate(n, out=out)
+    b.record(stream)
+    torch.cuda.synchronize()
+    g.close()
+    s = a.elapsed_time(b) / 1e3 / reps
+    row = {"value": n / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": 1, "n": n,
+           "note": "one GPU thread; 10^6 dependent steps (latency-bound parity config)",
+           "paper_context": {"listing1_one_xeon_core_numbers_per_s": 1.38e8, "source": "PAPER.md P:1040-1041"}}
+    if with_oracle:
+        import oracle as O
+
+        st = O.init_states(P.V0, 0, 0, 1, paper_defaults=True)
+        t0 = time.perf_counter()
+        ref = O.generate(P.V0, st, n)
+        el = time.perf_counter() - t0
+        row["cpu_baseline"] = {"value": n / el, "unit": UNIT, "cores": 1, "cpu_model": cpu_model(),
+                               "kind": "oracle", "sample": "the whole C1 call (10^6 Listing-1 steps), once",
+                               "bit_exact_vs_gpu": bool(np.array_equal(ref.reshape(-1), first.reshape(-1)))}
+    return row
 
 
 def measure_c4_sharded(P, torch, dev):
@@ -686,6 +807,7 @@ def measure_secondary(P, torch, dev, args):
 
     if args.c5_only:
         return {"c5_consume_allreduce": measure_c5_sharded(P, torch, dev, timed)}
+    res["c1_v0"] = measure_c1(P, torch, dev, with_oracle=not args.no_cpu_baseline)
     if args.c4_only:
         return {"c4_sharded_1e12": measure_c4_sharded(P, torch, dev)}
     S, n = W.CONFIGS["C3"]["n_streams"], W.CONFIGS["C3"]["n"]
@@ -697,7 +819,7 @@ def measure_secondary(P, torch, dev, args):
     sq_peak = 148 * 4 * 32 * 1.965e9 / 8
     res["c3_v2_store"] = {"value": S * n / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S, "n": n,
                           "bbs_squarings_per_s": 12 * S * n / s,
-                          "heavy_fma_roofline": {"peak_squarings_per_s": sq_peak,
+                          "heavy_fma_model": {"peak_squarings_per_s": sq_peak,
                                                  "frac": 12 * S * n / s / sq_peak}}
     g.close()
     S0, n0 = 2**20, 128
@@ -730,7 +852,7 @@ def measure_secondary(P, torch, dev, args):
         res[name] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5,
                      "numbers_counted_exact": int(P.as_u64(st5)[2:].sum()) == 13 * S5 * n5}
         if var == P.V2:
-            res[name]["heavy_fma_roofline"] = {"peak_squarings_per_s": sq_peak, "frac": 12 * S5 * n5 / s / sq_peak}
+            res[name]["heavy_fma_model"] = {"peak_squarings_per_s": sq_peak, "frac": 12 * S5 * n5 / s / sq_peak}
         g.close()
     res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
     res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
@@ -775,6 +897,32 @@ def measure_secondary(P, torch, dev, args):
     return res
 
 
+def maybe_self_launch(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script under
+    torch.distributed.run with N processes on this node (one per GPU, NCCL,
+    rendezvous on 127.0.0.1) and return its exit code.  None = run here."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return None
+    import socket
+    import subprocess
+
+    backend = os.environ.get("CIPRNG_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs for NCCL, found {have}\n")
+            return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -792,6 +940,9 @@ def main():
     ap.add_argument("--rounds", type=int, default=0, help="experiment override of numbers per stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    rc = maybe_self_launch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

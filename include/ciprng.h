@@ -72,7 +72,8 @@ enum prng_status {
     PRNG_ECUDA = -3,   /* CUDA runtime / driver error                 */
     PRNG_EALIGN = -4,  /* out_dev not 16-byte aligned when required   */
     PRNG_ESIZE = -5,   /* size overflow (n * n_local * 4 > SIZE_MAX)   */
-    PRNG_ESTATE = -6   /* state buffer size mismatch (get/set_state)  */
+    PRNG_ESTATE = -6   /* state buffer size mismatch (get/set_state), or
+                          set_state content invalid (see prng_set_state) */
 };
 
 /* Store path of prng_generate (tuning knob; every path is bit-identical). */
@@ -294,7 +295,10 @@ CIPRNG_API int prng_get_info(const prng_t *h, prng_info_t *info);
  *  V3 (4):  a.lo a.hi (xor64) | x | tp
  *  V4 (24): V0's 22 generator words | x | tp
  * get/set copy exactly state_words*n_local*4 bytes (else PRNG_ESTATE) and
- * synchronise the device.  set_state is the checkpoint-resume hook (P:905:
+ * synchronise the device.  set_state validates the content on the host
+ * before any copy and returns PRNG_ESTATE (device state untouched) if a V2
+ * modulus index m_j >= 78, a V2 state y_j >= its modulus, or any
+ * xorshift-family generator of V0/V1/V3/V4 is all zero (a fixed point).  set_state is the checkpoint-resume hook (P:905:
  * the state written back after every kernel is a checkpoint). */
 CIPRNG_API int prng_get_state(const prng_t *h, void *host_buf, size_t bytes);
 CIPRNG_API int prng_set_state(prng_t *h, const void *host_buf, size_t bytes);

@@ -69,6 +69,11 @@ class ChaoticPRNG:
         self.first, self.n_local, self.n_streams = first, n_local, n_streams
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
         self._comb = None if comb is None else np.ascontiguousarray(comb, dtype=np.uint8)
+        if self._comb is not None:
+            # prng_create_shard reads ntab * C bytes from this host pointer
+            ntab = 16 if variant == V2 else 2
+            _require(self._comb.size == ntab * (comb_size or 32),
+                     f"comb must hold {ntab} x comb_size = {ntab * (comb_size or 32)} entries, got {self._comb.size}")
         cfg = PrngConfig(
             comb_size=comb_size or 0,
             comb=None if self._comb is None else self._comb.ctypes.data,
@@ -140,6 +145,8 @@ class ChaoticPRNG:
         return buf
 
     def set_state(self, planes: np.ndarray) -> None:
+        """Checkpoint resume: SoA planes uint32 [state_words, n_local]; the
+        library rejects (PrngError, PRNG_ESTATE) a wrong size or invalid content."""
         buf = np.ascontiguousarray(planes, dtype=np.uint32)
         check(lib().prng_set_state(self._h, ctypes.c_void_p(buf.ctypes.data), buf.nbytes), "prng_set_state")
 

@@ -661,10 +661,51 @@ int prng_get_state(const prng_t *h, void *host_buf, size_t bytes) {
     return PRNG_OK;
 }
 
+/* Content check of a checkpoint before it reaches the device (the buffer is
+ * already on the host): a V2 modulus index must address the table and each
+ * BBS state must be a residue of its modulus (the kernels' Barrett squaring
+ * assumes y < M < 2^16, and an index past the table would read out of
+ * bounds); no xorshift-family generator may be all zero (a fixed point). */
+static bool state_valid(const prng_t *h, const uint32_t *st) {
+    const uint64_t L = h->n_local;
+    auto w = [&](int plane, uint64_t s) { return st[(uint64_t)plane * L + s]; };
+    auto zero = [&](int p0, int np, uint64_t s) {
+        uint32_t o = 0;
+        for (int p = p0; p < p0 + np; ++p) o |= w(p, s);
+        return o == 0;
+    };
+    std::vector<uint32_t> tab;
+    if (h->variant == PRNG_V2_BBS_COMB) tab = modulus_table();
+    for (uint64_t s = 0; s < L; ++s) {
+        switch (h->variant) {
+            case PRNG_V0_XORLIKE3:
+            case PRNG_V4_XORLIKE3_COMB:
+                if (zero(0, 2, s) || zero(2, 8, s) || zero(10, 10, s)) return false;
+                break;
+            case PRNG_V1_XOR128_COMB:
+                if (zero(0, 4, s)) return false;
+                break;
+            case PRNG_V3_XOR64_COMB:
+                if (zero(0, 2, s)) return false;
+                break;
+            case PRNG_V2_BBS_COMB:
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t m = w(8 + j, s);
+                    if (m >= h->n_mod || w(j, s) >= tab[(size_t)m * kModWords + 4]) return false;
+                }
+                break;
+            default:
+                return false;
+        }
+    }
+    return true;
+}
+
 int prng_set_state(prng_t *h, const void *host_buf, size_t bytes) {
     if (!h || !host_buf) return PRNG_EINVAL;
     const size_t need = (size_t)kStateWords[h->variant] * h->n_local * 4;
     if (bytes != need) return PRNG_ESTATE;
+    if (!state_valid(h, (const uint32_t *)host_buf)) return PRNG_ESTATE;
     DeviceGuard g(h->device);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(h->state, host_buf, need, cudaMemcpyHostToDevice));
@@ -679,7 +720,7 @@ const char *prng_strerror(int status) {
         case PRNG_ECUDA: return "CUDA error (see prng_last_cuda_error)";
         case PRNG_EALIGN: return "output pointer not 16-byte aligned";
         case PRNG_ESIZE: return "size overflow";
-        case PRNG_ESTATE: return "state buffer size mismatch";
+        case PRNG_ESTATE: return "state buffer size mismatch or invalid state content";
         default: return "unknown status";
     }
 }

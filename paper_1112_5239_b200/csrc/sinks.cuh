@@ -209,7 +209,7 @@ struct StatsSink {
         __syncthreads();
         // fold warp histograms, then one atomic per bin per CTA
         for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) {
-            uint32_t acc = 0;
+            uint64_t acc = 0;  // per-warp bins may each approach 2^31 before a flush
             for (uint32_t w = 0; w < nw; ++w) acc += all[256u * w + b];
             if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 2 + b), (unsigned long long)acc);
         }

@@ -29,11 +29,19 @@ def shard_range(n_streams: int, world_size: int, rank: int, align: int = 32) -> 
     return first_g * align, n_g * align
 
 
+# number of all-reduces that actually ran a collective (world size > 1) in
+# this process -- lets tests assert the exchange step really executed
+COLLECTIVES_RUN = 0
+
+
 def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
     """In-place SUM all-reduce of an int64 tensor (u64 bit patterns wrap the
-    same way under two's complement addition).  No-op without a process group."""
+    same way under two's complement addition).  No-op without a process group
+    or at world size 1 (there is nothing to exchange)."""
+    global COLLECTIVES_RUN
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        COLLECTIVES_RUN += 1
     return t
 
 

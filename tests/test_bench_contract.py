@@ -32,3 +32,24 @@ def test_reference_arm_line():
 
 def test_reference_arm_nonzero_rank_is_silent():
     assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}) == []
+
+
+def test_reference_arm_same_config_as_ours():
+    """The reference arm times the oracle on OUR arm's workload: every step a
+    full C2 call (2^20 streams x 128), CPU model named."""
+    d = json.loads(_run(args=("--steps", "1"))[0])
+    assert d["config"]["same_config_as_ours"] is True
+    assert (d["config"]["streams_per_gpu"], d["config"]["n_per_stream"]) == (2**20, 128)
+    assert "cpu_model" in d["cpu_baseline"]
+
+
+def test_gpus_n_without_torchrun_fails_loudly_without_gpus():
+    """`bench.py --gpus N` outside torchrun re-launches itself with N NCCL
+    ranks -- and refuses (non-zero exit, a message) when this node has fewer
+    than N GPUs (here: none)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.pop("CIPRNG_BENCH_BACKEND", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "needs 2 GPUs" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]

@@ -84,3 +84,21 @@ def test_theorem2_uniformity_by_sampling():
         hist = torch.bincount(out[:, 16::4].reshape(-1).long(), minlength=V).cpu().numpy()
         p[name] = chisquare(hist).pvalue
     assert p["negation"] > 1e-4 and p["unbalanced"] < 1e-12, p
+
+
+def test_alg1_and_gamma_validate_arguments():
+    """The kernels index z/x up to z.numel() - 1 and f up to 2^n - 1, so the
+    binding rejects short, mistyped or non-contiguous tensors before launch."""
+    z = torch.ones(64, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        C.alg1_generate(8, 4, z, torch.zeros(63, dtype=torch.int32, device="cuda"), 4)
+    with pytest.raises(ValueError):
+        C.alg1_generate(8, 4, z, torch.zeros(64, dtype=torch.int64, device="cuda"), 4)
+    with pytest.raises(ValueError):
+        C.alg1_generate(8, 4, z, torch.zeros(128, dtype=torch.int32, device="cuda")[::2], 4)
+    with pytest.raises(ValueError):
+        C.alg1_generate(8, 4, z, torch.zeros(64, dtype=torch.int32, device="cuda"), 4,
+                         f=torch.zeros(255, dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        C.gamma_check(6, f=torch.zeros(32, dtype=torch.int32, device="cuda"))
+    assert C.gamma_check(4, f=torch.arange(16, dtype=torch.int32, device="cuda") ^ 15)["chaotic"]

@@ -151,6 +151,67 @@ def test_v1_generate_host_matches_device():
         assert np.array_equal(dev, host)
 
 
+@pytest.mark.parametrize("variant,n", [(W.V1, 128), (W.V1, 256), (W.V1, 36), (W.V2, 128), (W.V3, 128)])
+def test_generate_host_multi_chunk(variant, n):
+    """prng_generate_host over MORE than one ~64 MiB chunk: the staging double
+    buffer with its ev_gen / ev_copy waits, and the store kernels launched
+    with s_begin != 0 into a chunk-sized tensor map -- 2^18 + 32 streams, so
+    the last chunk is 32 rows (a multiple of 32, not of 64); n = 256 takes the
+    3-D band kernel, n = 36 the staged path.  Two calls equal prng_generate
+    word for word, and the ragged last group equals the oracle."""
+    S = 2**18 + 32
+    g1 = P.ChaoticPRNG(SEEDS[0], S, variant)
+    g2 = P.ChaoticPRNG(SEEDS[0], S, variant)
+    st = O.init_states(variant, SEEDS[0], S - 32, 32)
+    host = torch.empty((S, n), dtype=torch.int32, pin_memory=True)
+    for _ in range(2):
+        dev = P.as_u32(g1.generate(n))
+        g2.generate_host(n, out=host)
+        hv = host.numpy().view(np.uint32)
+        assert g2.info().kernel_launches >= 3
+        assert np.array_equal(dev, hv), first_mismatch(hv, dev)
+        ref = O.generate(variant, st, n)
+        assert np.array_equal(hv[S - 32:], ref), first_mismatch(hv[S - 32:], ref)
+    assert np.array_equal(g1.get_state(), g2.get_state())
+    g1.close()
+    g2.close()
+
+
+def test_set_state_rejects_invalid_content():
+    """prng_set_state validates a checkpoint on the host before copying it:
+    a V2 modulus index past the 78-entry table, a V2 state >= its modulus, an
+    all-zero xorshift generator -- PrngError, device state unchanged."""
+    g = P.ChaoticPRNG(3, 64, W.V2)
+    good = g.get_state()
+    for plane, col, val in ((8, 5, 78), (8, 0, 2**31), (3, 7, 59989 + 1)):
+        bad = good.copy()
+        if plane == 3:      # y >= M: use the instance's own modulus
+            bad[3, col] = O.moduli()[int(good[8 + 3, col])]
+        else:
+            bad[plane, col] = val
+        with pytest.raises(P.PrngError):
+            g.set_state(bad)
+        assert np.array_equal(g.get_state(), good)
+    g.set_state(good)
+    for variant, planes in ((W.V1, range(0, 4)), (W.V3, range(0, 2)), (W.V0, range(2, 10)), (W.V4, range(10, 20))):
+        h = P.ChaoticPRNG(3, 64, variant)
+        st = h.get_state()
+        bad = st.copy()
+        bad[list(planes), 17] = 0
+        with pytest.raises(P.PrngError):
+            h.set_state(bad)
+        assert np.array_equal(h.get_state(), st)
+        h.close()
+    g.close()
+
+
+def test_comb_table_size_checked():
+    with pytest.raises(ValueError):
+        P.ChaoticPRNG(0, 64, W.V2, comb_size=4, comb=np.zeros(8, np.uint8))   # V1-shaped table for V2
+    with pytest.raises(ValueError):
+        P.ChaoticPRNG(0, 64, W.V1, comb_size=4, comb=np.zeros(7, np.uint8))
+
+
 def test_v1_set_state_resume():
     """Checkpoint/resume (the written-back state is a checkpoint)."""
     g = P.ChaoticPRNG(5, 256, W.V1)

@@ -1,12 +1,19 @@
-"""Fused-consumer run over the process group (BASELINE configs[4] shape):
-each rank consumes its shard of the stream space on its own GPU, then one
-NCCL all-reduce of the 258 u64 statistics.
+"""Sharded consumer + verification digests over the process group (the a7
+row; BASELINE configs[4] shape by default): each rank consumes its shard of
+the stream space on its own GPU through dist.sharded_consume (prng_consume,
+then one SUM all-reduce of the 258 u64 statistics), then, from fresh
+handles, runs dist.sharded_digests (prng_generate + prng_digest per call,
+digests summed across ranks).
 
   torchrun --nproc-per-node G --master-addr 127.0.0.1 tools/dist_consume.py \
-      [--streams 8388608] [--n 1024] [--calls 16] [--variant 1]
+      [--streams 8388608] [--rounds 1024] [--calls 16] [--variant 1] \
+      [--backend nccl|gloo] [--digest-calls 0]
 
-Rank 0 prints JSON: stats digest, pi estimate, chi-square p of the top-byte
-histogram, consumer throughput (max over ranks, CUDA events), stats list.
+gloo lets several ranks share one GPU (CUDA tensors, host-staged reduce);
+NCCL needs one GPU per rank.  Rank 0 prints JSON: the reduced statistics,
+the digest list, pi estimate, chi-square p of the top-byte histogram,
+consumer throughput (max over ranks, CUDA events) and how many all-reduces
+actually ran a collective on this rank.
 """
 from __future__ import annotations
 
@@ -24,8 +31,8 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_1112_5239_b200 as P  # noqa: E402
+import paper_1112_5239_b200.dist as D  # noqa: E402
 import workloads as W  # noqa: E402
-from paper_1112_5239_b200.dist import allreduce_sum_, shard_range  # noqa: E402
 
 
 def main():
@@ -35,28 +42,31 @@ def main():
     ap.add_argument("--calls", type=int, default=W.CONFIGS["C5"]["calls"])
     ap.add_argument("--variant", type=int, default=1)
     ap.add_argument("--seed", type=int, default=W.SEEDS[0])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--digest-calls", type=int, default=0)
     args = ap.parse_args()
     lr = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(lr)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    dev = lr % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo")
     ws, rk = dist.get_world_size(), dist.get_rank()
-    first, n_local = shard_range(args.streams, ws, rk)
-    g = P.ChaoticPRNG(args.seed, args.streams, args.variant, shard=(first, n_local))
-    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
-    g.consume(2, torch.zeros_like(stats))  # warm-up on a scratch buffer (state advances: re-create)
-    g.close()
-    g = P.ChaoticPRNG(args.seed, args.streams, args.variant, shard=(first, n_local))
+    nccl_version = ".".join(map(str, torch.cuda.nccl.version())) if args.backend == "nccl" else None
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.calls):
-        g.consume(args.rounds, stats)
-    allreduce_sum_(stats)
+    stats = D.sharded_consume(args.seed, args.streams, args.variant, args.rounds, args.calls)
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    if args.backend == "gloo":
+        t = t.cpu()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    digs = D.sharded_digests(args.seed, args.streams, args.variant, args.rounds, args.digest_calls) \
+        if args.digest_calls else []
     s = P.as_u64(stats)
     if rk == 0:
         from scipy import stats as sst
@@ -67,15 +77,16 @@ def main():
         exp = hist.sum() / 256
         chi2 = float(((hist - exp) ** 2 / exp).sum())
         print(json.dumps({
-            "world_size": ws, "variant": args.variant, "streams": args.streams, "n": args.rounds, "calls": args.calls,
+            "world_size": ws, "backend": args.backend, "nccl_version": nccl_version, "variant": args.variant,
+            "seed": args.seed, "streams": args.streams, "n": args.rounds, "calls": args.calls,
             "numbers": args.streams * args.rounds * args.calls,
             "seconds_max_over_ranks": float(t.item()),
             "numbers_per_s": args.streams * args.rounds * args.calls / float(t.item()),
             "pi_hat": 4 * inside / pairs, "pi_z": (inside / pairs - p) / math.sqrt(p * (1 - p) / pairs),
             "hist_chi2_p": float(sst.chi2.sf(chi2, 255)),
-            "stats": [int(v) for v in s],
+            "collectives_run": D.COLLECTIVES_RUN,
+            "stats": [int(v) for v in s], "digests": digs,
         }))
-    g.close()
     dist.destroy_process_group()
 
 
