@@ -72,8 +72,18 @@ enum prng_status {
     PRNG_ECUDA = -3,   /* CUDA runtime / driver error                 */
     PRNG_EALIGN = -4,  /* out_dev not 16-byte aligned when required   */
     PRNG_ESIZE = -5,   /* size overflow (n * n_local * 4 > SIZE_MAX)   */
-    PRNG_ESTATE = -6   /* state buffer size mismatch (get/set_state), or
+    PRNG_ESTATE = -6,  /* state buffer size mismatch (get/set_state), or
                           set_state content invalid (see prng_set_state) */
+    PRNG_EIO = -7      /* prng_emit: a write to the sink failed (errno is
+                          left as write(2) set it)                    */
+};
+
+/* Serialisation formats of prng_emit. */
+enum prng_emit_format {
+    PRNG_EMIT_RAW_LE32 = 0, /* 4 bytes per word, little-endian u32         */
+    PRNG_EMIT_HEX = 1,      /* "%08x\n": 8 lowercase hex digits + newline   */
+    PRNG_EMIT_BITS = 2      /* 32 ASCII '0'/'1', most significant bit first
+                               (reading Q31), + newline                     */
 };
 
 /* Store path of prng_generate (tuning knob; every path is bit-identical). */
@@ -159,6 +169,25 @@ CIPRNG_API int prng_generate(prng_t *h, uint64_t n_per_stream, uint32_t *out_dev
  * SYNCHRONOUS: returns after the last word has landed in out_host. */
 CIPRNG_API int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *out_host, void *stream);
 
+/* Emitter for external test batteries (SURVEY s8(b) raw-LE32 sink; SPEC
+ * S:378 "raw little-endian 32-bit words to file or standard output",
+ * S:642-650 emit(generator, count, format); the paper fed its outputs to
+ * DieHARD / TestU01 BigCrush).  Runs ONE call of n rounds --
+ * the same words and state evolution as prng_generate -- and writes the
+ * words in prng_generate's order (stream-major: local stream s, then round
+ * i) to the open file descriptor `fd` (1 = standard output) in `format`
+ * (enum prng_emit_format).  Pipeline: stream-range chunks of ~64 MiB of
+ * serialised bytes are generated (and, for the text formats, formatted by a
+ * kernel) on `stream`, copied to pinned host buffers owned by the handle on
+ * an internal copy stream, and written by the calling thread while the next
+ * chunk is generated.  SYNCHRONOUS.  *bytes_written (may be NULL) = bytes
+ * successfully written.  n == 0 writes nothing.  Errors: PRNG_EINVAL (NULL
+ * handle, fd < 0, unknown format), PRNG_ESIZE, PRNG_ENOMEM, PRNG_ECUDA,
+ * PRNG_EIO (a write failed: the remaining chunks are still generated, so the
+ * state has advanced by the whole call, but not written). */
+CIPRNG_API int prng_emit(prng_t *h, uint64_t n_per_stream, int fd, int format, uint64_t *bytes_written,
+                         void *stream);
+
 /* Fused consumer mode (the paper removes the store; statistics
  * are reading Q24): run the same n rounds as prng_generate -- identical
  * state evolution -- but use every x in-kernel instead of storing it, and
@@ -191,10 +220,15 @@ CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_de
  * PRNG_ECUDA. */
 CIPRNG_API int prng_battery(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
 
-/* Verification digest of one call's output block (reading Q28):
- * digest_dev[0] += sum over s < n_local, i < n of
- *   mix64(mix64((first_stream + s) * n + i) ^ out_dev[s*n + i])  (mod 2^64),
- * mix64 = SplitMix64 finaliser.  Position-aware and additive across shards. */
+/* Verification digest of one call's output block (reading Q28; a check
+ * value defined by this build, the paper has none):
+ * digest_dev[0] += sum over s < n_local, i < n of h(idx, out_dev[s*n + i])
+ *   (mod 2^64), idx = (first_stream + s) * n + i,
+ *   h(idx, x) = m(idx * 0x9E3779B97F4A7C15 + x),
+ *   m(z) = z ^= z >> 32; z *= 0xD6E8FEB86659FD93; z ^= z >> 32.
+ * Position-aware, additive across shards, and a bijection of each word for a
+ * fixed position (one wrong word always changes the digest).  out_dev needs
+ * only 4-byte alignment.  Errors: PRNG_EINVAL (NULL), PRNG_ECUDA. */
 CIPRNG_API int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n,
                 uint64_t *digest_dev, void *stream);
 

@@ -1024,15 +1024,25 @@ int orc_gamma_reach(const uint32_t *f, uint32_t n, uint64_t *report)
     return ORC_OK;
 }
 
-/* Verification digest (reading Q28): sum over the call's words of
- * mix64(mix64(idx) ^ x_idx) mod 2^64, idx = (first_stream + s) * n + i. */
+/* Verification digest (reading Q28, r2 definition): sum over the call's
+ * words of h(idx, x_idx) mod 2^64, idx = (first_stream + s) * n + i,
+ * h(idx, x) = m(idx * 0x9E3779B97F4A7C15 + x),
+ * m(z) = z ^= z >> 32; z *= 0xD6E8FEB86659FD93; z ^= z >> 32. */
+static uint64_t orc_digest_mix(uint64_t z)
+{
+    z ^= z >> 32;
+    z *= 0xD6E8FEB86659FD93ull;
+    z ^= z >> 32;
+    return z;
+}
+
 uint64_t orc_digest_words(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n)
 {
     uint64_t s, i, acc = 0;
     for (s = 0; s < n_local; s++)
         for (i = 0; i < n; i++) {
             uint64_t idx = (first_stream + s) * n + i;
-            acc += orc_mix64(orc_mix64(idx) ^ (uint64_t)out[s * n + i]);
+            acc += orc_digest_mix(idx * 0x9E3779B97F4A7C15ull + (uint64_t)out[s * n + i]);
         }
     return acc;
 }

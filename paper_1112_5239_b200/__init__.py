@@ -11,11 +11,13 @@ fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
 
 from ._lib import (  # noqa: F401
+    EMIT_FORMATS,
     STORE_AUTO,
     STORE_DIRECT,
     STORE_TMA,
@@ -108,6 +110,30 @@ class ChaoticPRNG:
         check(lib().prng_generate_host(self._h, n, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
               "prng_generate_host")
         return out
+
+    def emit(self, n: int, sink, format: str = "raw-le32", stream=None) -> int:
+        """One call of n rounds serialised to `sink` (an int file descriptor,
+        a path, or a file object with fileno(); include/ciprng.h prng_emit):
+        format "raw-le32", "hex" or "bits".  Returns the bytes
+        written; the words are prng_generate's, in its order."""
+        _require(format in EMIT_FORMATS, f"format must be one of {sorted(EMIT_FORMATS)}")
+        close = False
+        if isinstance(sink, int):
+            fd = sink
+        elif isinstance(sink, (str, bytes)) or hasattr(sink, "__fspath__"):
+            fd = os.open(sink, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+            close = True
+        else:
+            sink.flush()
+            fd = sink.fileno()
+        written = ctypes.c_uint64(0)
+        try:
+            check(lib().prng_emit(self._h, n, fd, EMIT_FORMATS[format], ctypes.byref(written),
+                                  _stream_handle(stream)), "prng_emit")
+        finally:
+            if close:
+                os.close(fd)
+        return written.value
 
     def consume(self, n: int, stats: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Fused consumer: adds {inside, pairs, hist[256]} into int64 [258] (u64 bits)."""
@@ -208,6 +234,10 @@ def prng_generate(h: ChaoticPRNG, n_per_stream: int, out=None, stream=None):
 
 def prng_generate_host(h: ChaoticPRNG, n_per_stream: int, out=None, stream=None):
     return h.generate_host(n_per_stream, out=out, stream=stream)
+
+
+def prng_emit(h: ChaoticPRNG, n_per_stream: int, sink, format: str = "raw-le32", stream=None) -> int:
+    return h.emit(n_per_stream, sink, format, stream=stream)
 
 
 def prng_consume(h: ChaoticPRNG, n_per_stream: int, stats=None, stream=None):

@@ -11,8 +11,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libciprng.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ciprng.h")
 
-PRNG_OK, PRNG_EINVAL, PRNG_ENOMEM, PRNG_ECUDA, PRNG_EALIGN, PRNG_ESIZE, PRNG_ESTATE = 0, -1, -2, -3, -4, -5, -6
+PRNG_OK, PRNG_EINVAL, PRNG_ENOMEM, PRNG_ECUDA, PRNG_EALIGN, PRNG_ESIZE, PRNG_ESTATE, PRNG_EIO = \
+    0, -1, -2, -3, -4, -5, -6, -7
 STORE_AUTO, STORE_DIRECT, STORE_TMA = 0, 1, 2
+EMIT_FORMATS = {"raw-le32": 0, "hex": 1, "bits": 2}
 
 
 class PrngConfig(ctypes.Structure):
@@ -67,6 +69,7 @@ def lib() -> ctypes.CDLL:
             "prng_destroy": ([vp], i32),
             "prng_generate": ([vp, u64, vp, vp], i32),
             "prng_generate_host": ([vp, u64, vp, vp], i32),
+            "prng_emit": ([vp, u64, i32, i32, ctypes.POINTER(u64), vp], i32),
             "prng_consume": ([vp, u64, vp, vp], i32),
             "prng_battery": ([vp, u64, vp, vp], i32),
             "prng_cbg_encrypt": ([i32, u64, u64, vp, vp, vp, vp, vp, vp, vp], i32),

@@ -6,7 +6,9 @@
 #include <tuple>
 #include <cstdio>
 #include <cstdlib>
+#include <cerrno>
 #include <cstring>
+#include <unistd.h>
 #include <vector>
 
 #include "../../include/ciprng.h"
@@ -177,6 +179,11 @@ struct prng_s {
     size_t staging_words = 0;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_gen[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+    // emitter (prng_emit): device text buffers and pinned host buffers
+    uint8_t *text[2] = {nullptr, nullptr};
+    size_t text_bytes = 0;
+    uint8_t *pinned[2] = {nullptr, nullptr};
+    size_t pinned_bytes = 0;
 };
 
 namespace {
@@ -485,11 +492,43 @@ int prng_destroy(prng_t *h) {
     cudaFree(h->staging[0]);
     cudaFree(h->staging[1]);
     for (int b = 0; b < 2; ++b) {
+        cudaFree(h->text[b]);
+        if (h->pinned[b]) cudaFreeHost(h->pinned[b]);
+    }
+    for (int b = 0; b < 2; ++b) {
         if (h->ev_gen[b]) cudaEventDestroy(h->ev_gen[b]);
         if (h->ev_copy[b]) cudaEventDestroy(h->ev_copy[b]);
     }
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     delete h;
+    return PRNG_OK;
+}
+
+// Device staging (two chunk buffers of `words` u32) and the copy stream +
+// events of the host pipelines (prng_generate_host, prng_emit).
+static int ensure_pipeline(prng_t *h, size_t words) {
+    if (words > h->staging_words) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(h->staging[b]);
+            h->staging[b] = nullptr;
+        }
+        h->staging_words = 0;
+        for (int b = 0; b < 2; ++b) {
+            cudaError_t e = cudaMalloc(&h->staging[b], words * 4);
+            if (e != cudaSuccess) {
+                cuda_fail(e);
+                return PRNG_ENOMEM;
+            }
+        }
+        h->staging_words = words;
+    }
+    if (!h->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&h->ev_gen[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_copy[b], cudaEventDisableTiming));
+        }
+    }
     return PRNG_OK;
 }
 
@@ -523,29 +562,8 @@ int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *out_host, voi
     uint64_t rows = (64ull << 20) / row_bytes;
     rows = std::max<uint64_t>(64, rows / 64 * 64);
     if (rows > h->n_local) rows = h->n_local;
-    const size_t need = (size_t)rows * n_per_stream;
-    if (need > h->staging_words) {
-        for (int b = 0; b < 2; ++b) {
-            cudaFree(h->staging[b]);
-            h->staging[b] = nullptr;
-        }
-        h->staging_words = 0;
-        for (int b = 0; b < 2; ++b) {
-            cudaError_t e = cudaMalloc(&h->staging[b], need * 4);
-            if (e != cudaSuccess) {
-                cuda_fail(e);
-                return PRNG_ENOMEM;
-            }
-        }
-        h->staging_words = need;
-    }
-    if (!h->copy_stream) {
-        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-        for (int b = 0; b < 2; ++b) {
-            CK(cudaEventCreateWithFlags(&h->ev_gen[b], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&h->ev_copy[b], cudaEventDisableTiming));
-        }
-    }
+    rc = ensure_pipeline(h, (size_t)rows * n_per_stream);
+    if (rc) return rc;
     uint32_t launches = 0;
     uint64_t chunk = 0;
     for (uint64_t r0 = 0; r0 < h->n_local; r0 += rows, ++chunk) {
@@ -566,6 +584,98 @@ int prng_generate_host(prng_t *h, uint64_t n_per_stream, uint32_t *out_host, voi
     CK(cudaStreamSynchronize(h->copy_stream));
     CK(cudaStreamSynchronize(st));
     return PRNG_OK;
+}
+
+static bool write_all(int fd, const uint8_t *p, size_t len) {
+    while (len) {
+        const ssize_t k = ::write(fd, p, len);
+        if (k < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        p += k;
+        len -= (size_t)k;
+    }
+    return true;
+}
+
+int prng_emit(prng_t *h, uint64_t n_per_stream, int fd, int format, uint64_t *bytes_written, void *stream) {
+    if (bytes_written) *bytes_written = 0;
+    if (!h || fd < 0 || format < PRNG_EMIT_RAW_LE32 || format > PRNG_EMIT_BITS) return PRNG_EINVAL;
+    h->last_launches = 0;
+    if (n_per_stream == 0) return PRNG_OK;
+    const uint64_t bpw = format == PRNG_EMIT_RAW_LE32 ? 4 : format == PRNG_EMIT_HEX ? 9 : 33;
+    if (h->n_local > SIZE_MAX / bpw / n_per_stream) return PRNG_ESIZE;
+    DeviceGuard g(h->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    // chunk = whole 64-stream tiles, about 64 MiB of serialised bytes
+    uint64_t rows = (64ull << 20) / (n_per_stream * bpw);
+    rows = std::max<uint64_t>(64, rows / 64 * 64);
+    if (rows > h->n_local) rows = h->n_local;
+    const size_t words = (size_t)rows * n_per_stream, bytes = words * bpw;
+    int rc = ensure_pipeline(h, words);
+    if (rc) return rc;
+    if (format != PRNG_EMIT_RAW_LE32 && bytes > h->text_bytes) {
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(h->text[b]);
+            h->text[b] = nullptr;
+        }
+        h->text_bytes = 0;
+        for (int b = 0; b < 2; ++b)
+            if (cudaMalloc(&h->text[b], bytes) != cudaSuccess) return PRNG_ENOMEM;
+        h->text_bytes = bytes;
+    }
+    if (bytes > h->pinned_bytes) {
+        for (int b = 0; b < 2; ++b) {
+            if (h->pinned[b]) cudaFreeHost(h->pinned[b]);
+            h->pinned[b] = nullptr;
+        }
+        h->pinned_bytes = 0;
+        for (int b = 0; b < 2; ++b)
+            if (cudaHostAlloc(reinterpret_cast<void **>(&h->pinned[b]), bytes, cudaHostAllocDefault) != cudaSuccess)
+                return PRNG_ENOMEM;
+        h->pinned_bytes = bytes;
+    }
+    // chunk c: generate (+ format) on `stream`, copy to pinned[c & 1] on the
+    // copy stream; meanwhile the host writes chunk c - 1.  Every chunk is
+    // generated even after a write failure, so the handle's state always
+    // advances by the whole call (like prng_generate).
+    uint32_t launches = 0;
+    uint64_t written = 0, pend_bytes = 0;
+    bool io_ok = true;
+    int pend = -1;  // buffer of the chunk waiting to be written
+    uint64_t chunk = 0;
+    for (uint64_t r0 = 0; r0 < h->n_local; r0 += rows, ++chunk) {
+        const int b = (int)(chunk & 1);
+        const uint64_t cnt = std::min<uint64_t>(rows, h->n_local - r0);
+        if (chunk >= 2) CK(cudaStreamWaitEvent(st, h->ev_copy[b], 0));
+        h->last_launches = 0;
+        rc = run_pass(h, n_per_stream, r0, cnt, h->staging[b], nullptr, 0, st);
+        if (rc) return rc;
+        launches += h->last_launches;
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(h->staging[b]);
+        if (format != PRNG_EMIT_RAW_LE32) {
+            launches += launch_format(h->staging[b], cnt * n_per_stream, format, h->text[b], st);
+            CK(cudaGetLastError());
+            src = h->text[b];
+        }
+        CK(cudaEventRecord(h->ev_gen[b], st));
+        CK(cudaStreamWaitEvent(h->copy_stream, h->ev_gen[b], 0));
+        CK(cudaMemcpyAsync(h->pinned[b], src, cnt * n_per_stream * bpw, cudaMemcpyDeviceToHost, h->copy_stream));
+        CK(cudaEventRecord(h->ev_copy[b], h->copy_stream));
+        if (pend >= 0) {
+            CK(cudaEventSynchronize(h->ev_copy[pend]));
+            if (io_ok && (io_ok = write_all(fd, h->pinned[pend], pend_bytes))) written += pend_bytes;
+        }
+        pend = b;
+        pend_bytes = cnt * n_per_stream * bpw;
+    }
+    CK(cudaEventSynchronize(h->ev_copy[pend]));
+    if (io_ok && (io_ok = write_all(fd, h->pinned[pend], pend_bytes))) written += pend_bytes;
+    CK(cudaStreamSynchronize(st));
+    h->last_launches = launches;
+    if (bytes_written) *bytes_written = written;
+    return io_ok ? PRNG_OK : PRNG_EIO;
 }
 
 int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream) {
@@ -721,6 +831,7 @@ const char *prng_strerror(int status) {
         case PRNG_EALIGN: return "output pointer not 16-byte aligned";
         case PRNG_ESIZE: return "size overflow";
         case PRNG_ESTATE: return "state buffer size mismatch or invalid state content";
+        case PRNG_EIO: return "write to the output sink failed (see errno)";
         default: return "unknown status";
     }
 }

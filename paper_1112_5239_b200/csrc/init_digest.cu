@@ -108,15 +108,71 @@ int launch_init(const InitArgs &a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ digest
+// Q28 (r2): d = sum_idx h(idx, x_idx) mod 2^64 with idx = global s*n + i and
+// h(idx, x) = m(idx * G + x), m(z) = { z ^= z >> 32; z *= K; z ^= z >> 32 }.
+// h is a bijection of x for a fixed idx (add, xorshift, odd multiply are all
+// invertible), so any single wrong word changes the digest.  Per word: one
+// 64-bit multiply (3 IMAD) and about 8 ALU ops -- about 9 TB/s of ALU
+// throughput on 148 SMs, above HBM, so the kernel streams at memory speed
+// (the r1 definition, two SplitMix64 finalisers per word, ran at 1.36 TB/s).
+// idx * G advances by G per word, so it is an add, not a multiply.
+constexpr uint64_t kDigestG = 0x9E3779B97F4A7C15ull, kDigestK = 0xD6E8FEB86659FD93ull;
+
+__device__ __forceinline__ uint64_t digest_mix(uint64_t z) {
+    z ^= z >> 32;
+    z *= kDigestK;
+    return z ^ (z >> 32);
+}
+
+__device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Thread t of the grid takes 16-byte chunks t, t + stride, ... (two in
+// flight per iteration); `head` scalar words before the first aligned chunk
+// and the ragged tail go to the first threads.
 __global__ void __launch_bounds__(256) digest_kernel(const uint32_t *__restrict__ out, uint64_t first_stream,
                                                      uint64_t total, uint64_t n, uint64_t *digest) {
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t base = first_stream * n;  // global index of out[0]
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(out) >> 2) & 3u);
+    const uint64_t head = total < (uint64_t)((4u - mis) & 3u) ? total : (uint64_t)((4u - mis) & 3u);
+    const uint64_t chunks = (total - head) >> 2;
+    const uint32_t *body = out + head;
     uint64_t acc = 0;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += stride)
-        acc += splitmix_fin(splitmix_fin(base + k) ^ (uint64_t)out[k]);
+    uint64_t c = tid;
+    for (; c + stride < chunks; c += 2 * stride) {
+        const uint4 v0 = ld_stream_v4(body + 4 * c);
+        const uint4 v1 = ld_stream_v4(body + 4 * (c + stride));
+        uint64_t g0 = (base + head + 4 * c) * kDigestG, g1 = (base + head + 4 * (c + stride)) * kDigestG;
+        acc += digest_mix(g0 + v0.x); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.y); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.z); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.w);
+        acc += digest_mix(g1 + v1.x); g1 += kDigestG;
+        acc += digest_mix(g1 + v1.y); g1 += kDigestG;
+        acc += digest_mix(g1 + v1.z); g1 += kDigestG;
+        acc += digest_mix(g1 + v1.w);
+    }
+    if (c < chunks) {
+        const uint4 v0 = ld_stream_v4(body + 4 * c);
+        uint64_t g0 = (base + head + 4 * c) * kDigestG;
+        acc += digest_mix(g0 + v0.x); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.y); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.z); g0 += kDigestG;
+        acc += digest_mix(g0 + v0.w);
+    }
+    // head words [0, head) and tail words [head + 4 chunks, total): at most 6
+    const uint64_t tail0 = head + 4 * chunks;
+    if (tid < head) acc += digest_mix((base + tid) * kDigestG + out[tid]);
+    if (tid < total - tail0) acc += digest_mix((base + tail0 + tid) * kDigestG + out[tail0 + tid]);
 #pragma unroll
     for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
     if ((threadIdx.x & 31u) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long *>(digest), (unsigned long long)acc);
@@ -126,7 +182,8 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
                   cudaStream_t st, int grid) {
     const uint64_t total = n_local * n;
     if (total == 0) return 0;
-    uint64_t blocks = (total + 255) / 256;
+    uint64_t blocks = (total / 8 + 255) / 256;  // two 16-byte chunks per thread per iteration
+    if (blocks < 1) blocks = 1;
     if (blocks > (uint64_t)grid) blocks = grid;
     launch_k(digest_kernel, dim3((int)blocks), dim3(256), 0, st, out, first_stream, total, n, digest);
     return 1;

@@ -149,5 +149,7 @@ int launch_alg1(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *z, uint32_t
 int launch_gamma(const uint32_t *f, uint32_t n, uint8_t *mark, unsigned long long *report, cudaStream_t st);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);
+// emit.cu: format 1 = hex lines (9 B per word), 2 = bit lines (33 B per word)
+int launch_format(const uint32_t *words, uint64_t count, int format, uint8_t *text, cudaStream_t st);
 
 }  // namespace ciprng

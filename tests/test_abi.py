@@ -26,7 +26,7 @@ def test_version_string():
 
 
 def test_strerror_covers_all_statuses():
-    for st in range(0, -7, -1):
+    for st in range(0, -8, -1):
         assert P.lib().prng_strerror(st) != b"unknown status"
 
 

@@ -374,6 +374,21 @@ def test_digest_shard_additive():
     swapped = out.copy()
     swapped[[0, 1]] = swapped[[1, 0]]
     assert O.digest(swapped) != O.digest(out)
+    swapped = out.copy()
+    swapped[5, [2, 3]] = swapped[5, [3, 2]]
+    assert swapped[5, 2] != swapped[5, 3] and O.digest(swapped) != O.digest(out)
+
+
+def test_digest_injective_in_word():
+    """Q28: for a fixed position h(idx, .) is a bijection of the word (add,
+    xorshift and odd multiply are invertible), so one wrong word always
+    changes the digest: 2^16 distinct words at one position, at two
+    positions, give 2^16 distinct digests."""
+    for first, n in ((0, 1), (12345, 7)):
+        words = np.arange(0, 2**32, 2**16, dtype=np.uint64).astype(np.uint32)
+        ds = {O.digest(np.array([[w]], np.uint32), first * n) for w in words} if n == 1 else \
+            {O.digest(np.full((1, n), w, np.uint32), first) for w in words[:4096]}
+        assert len(ds) == (len(words) if n == 1 else 4096)
 
 
 # ---------------------------------------------------------------- V3 / V4

@@ -155,11 +155,12 @@ def test_v1_generate_host_matches_device():
 def test_generate_host_multi_chunk(variant, n):
     """prng_generate_host over MORE than one ~64 MiB chunk: the staging double
     buffer with its ev_gen / ev_copy waits, and the store kernels launched
-    with s_begin != 0 into a chunk-sized tensor map -- 2^18 + 32 streams, so
-    the last chunk is 32 rows (a multiple of 32, not of 64); n = 256 takes the
+    with s_begin != 0 into a chunk-sized tensor map -- at least two full chunks
+    + 32 streams, so the last chunk is 32 rows (a multiple of 32, not of 64); n = 256 takes the
     3-D band kernel, n = 36 the staged path.  Two calls equal prng_generate
     word for word, and the ragged last group equals the oracle."""
-    S = 2**18 + 32
+    rows = (64 << 20) // (4 * n) // 64 * 64   # api.cu prng_generate_host chunk rows
+    S = max(2**18, 2 * rows) + 32
     g1 = P.ChaoticPRNG(SEEDS[0], S, variant)
     g2 = P.ChaoticPRNG(SEEDS[0], S, variant)
     st = O.init_states(variant, SEEDS[0], S - 32, 32)
@@ -362,6 +363,20 @@ def test_digest_matches_oracle():
     out = g.generate(33)
     d = int(P.as_u64(P.digest(out, first_stream=256))[0])
     assert d == O.digest(P.as_u32(out), 256)
+
+
+@pytest.mark.parametrize("rows,n", [(1, 1), (1, 3), (1, 6), (3, 5), (7, 9), (1000, 37), (4096, 128)])
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_digest_ragged_and_misaligned(rows, n, offset):
+    """The digest kernel's 16-byte vector body with its scalar head (output
+    views 4, 8, 12 bytes past a 16-byte boundary) and ragged tail (total
+    words not a multiple of 4 or of the 2-chunk unroll)."""
+    gen = W.rng(28)
+    buf = torch.from_numpy(W.random_words(gen, rows * n + offset).view(np.int32)).cuda()
+    view = buf[offset:].view(rows, n)
+    first = int(gen.integers(0, 2**20))
+    d = int(P.as_u64(P.digest(view, first_stream=first))[0])
+    assert d == O.digest(P.as_u32(view), first)
 
 
 # ------------------------------------------------------------- full configs
