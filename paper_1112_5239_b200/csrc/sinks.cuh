@@ -84,6 +84,30 @@ __device__ __forceinline__ void warp_hist_flush(uint32_t hist, uint64_t *gdst) {
 constexpr uint64_t kHistFlushAt = 1ull << 31;
 constexpr uint64_t kMaxRowsPerWarpTile = 64;  // the fast kernels' tile; others use 32
 
+#if !defined(CIPRNG_PAIR_ADDCC)
+// r2: v^2 + u^2 as ONE 64-bit multiply-add whose carry-out is the test --
+// the mad.lo.cc / madc.hi.cc chain compiles to IMAD.WIDE.U32 RZ, Pc, v, v, U
+// (carry into a predicate), and ptxas folds the counter updates of two pairs
+// into one IADD3.X cnt, RZ, RZ, cnt, Pc0, Pc1: per pair 2 IMAD.WIDE + 0.5
+// ALU instead of 2 IMAD.WIDE + 2.5 ALU (the add.cc form below).  Measured
+// (C5 shape, L2 flushed, profiles/experiments/s50_pair.jsonl): V1 consumer
+// 1.69 -> 1.81e12 numbers/s, V3 1.15 -> 1.20e12, V0 +1.5 %; V2 -1.3 % (its
+// heavy pipe is the binding one), so gen_v2.cu keeps the add.cc form
+// (CIPRNG_PAIR_ADDCC defined before this header).
+__device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_t v) {
+    asm("{\n\t"
+        ".reg .u64 U;\n\t"
+        ".reg .u32 ul, uh, d;\n\t"
+        "mul.wide.u32 U, %1, %1;\n\t"
+        "mov.b64 {ul, uh}, U;\n\t"
+        "mad.lo.cc.u32 d, %2, %2, ul;\n\t"
+        "madc.hi.cc.u32 d, %2, %2, uh;\n\t"
+        "addc.u32 %0, %0, 0;\n\t"
+        "}"
+        : "+r"(cnt)
+        : "r"(u), "r"(v));
+}
+#else
 __device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_t v) {
     asm("{\n\t"
         ".reg .u64 U, V;\n\t"
@@ -99,6 +123,7 @@ __device__ __forceinline__ void count_outside(uint32_t &cnt, uint32_t u, uint32_
         : "+r"(cnt)
         : "r"(u), "r"(v));
 }
+#endif
 // The same with the counter's add-with-carry as zero*zero + cnt + CF
 // (madc: IMAD.X on the FMA pipe instead of IADD3.X on the ALU pipe; `zero`
 // is GenArgs::zero, a 0 the compiler cannot fold).  Experiment only
