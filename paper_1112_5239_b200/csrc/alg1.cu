@@ -32,6 +32,12 @@ __device__ __forceinline__ uint32_t f_single(const uint32_t *f, uint32_t nmask, 
     return (x & ~bit) | (fx & bit);
 }
 
+// One thread per stream.  Outputs go out in 8-word chunks (two 16-byte
+// stores = one full 32-byte sector) when the rows allow it: r1 stored one
+// word per thread per output, rows n_out words apart, and ncu counted 110 MB
+// of partial-sector read-modify-write DRAM reads per launch
+// (profiles/r1zc_ncu_summary.md).  XORshift(n) for a power-of-two n (the
+// common cell counts) is a mask instead of a division by a runtime n.
 __global__ void __launch_bounds__(256) alg1_kernel(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *zs,
                                                    uint32_t *xs, uint64_t n_streams, uint64_t n_out,
                                                    uint32_t *out) {
@@ -40,15 +46,30 @@ __global__ void __launch_bounds__(256) alg1_kernel(const uint32_t *f, uint32_t n
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_streams) return;
     const uint32_t nmask = n == 32 ? 0xFFFFFFFFu : (1u << n) - 1u;
+    const bool n_pow2 = (n & (n - 1u)) == 0;
     uint32_t z = zs[s], x = xs[s];
-    for (uint64_t j = 0; j < n_out; ++j) {
+    uint32_t *row = out + s * n_out;
+    const bool vec8 = (n_out % 8 == 0) && (reinterpret_cast<uintptr_t>(out) % 32 == 0);
+    auto next = [&]() {
         const uint32_t k = b + 1u + xs32(z) % b;
         for (uint32_t i = 0; i <= k; ++i) {
-            const uint32_t cell = 1u + xs32(z) % n;
+            const uint32_t r = xs32(z);
+            const uint32_t cell = 1u + (n_pow2 ? (r & (n - 1u)) : r % n);
             x = f_single(f, nmask, cell, x);
         }
-        out[s * n_out + j] = x;
+        return x;
+    };
+    uint64_t j = 0;
+    if (vec8) {
+        for (; j < n_out; j += 8) {
+            uint32_t o[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = next();
+            st_v4(row + j, o[0], o[1], o[2], o[3]);
+            st_v4(row + j + 4, o[4], o[5], o[6], o[7]);
+        }
     }
+    for (; j < n_out; ++j) row[j] = next();
     zs[s] = z;
     xs[s] = x;
 }

@@ -8,9 +8,10 @@ produce the right words.  Shapes are tiny (a few tiles plus a ragged tail):
 the sanitizers slow kernels down by 10-1000x.
 
 Store paths covered (csrc/api.cu run_pass):
-  * 2-D TMA boxes (V1 n = 128, V3 n = 128), 16- and 8-round boxes, 1 and 3 buffers
+  * 2-D TMA boxes (V1 n = 128, V3 n = 128; any n % 4 == 0 with aligned rows),
+    16- and 8-round boxes, 1 and 3 buffers
   * 3-D band boxes (V1 n = 256)
-  * staged shared-memory + coalesced STG (V1 / V3 n = 36; misaligned output)
+  * staged shared-memory + coalesced STG (V1 / V3 n % 4 != 0; misaligned output)
   * direct 128-bit / scalar stores (STORE_DIRECT; V0, V2, V4)
 plus the fused consumer (V0..V4), the battery, generate_host, the digest,
 chaotic Blum-Goldwasser encrypt / decrypt, Algorithm 1 and the Gamma(f) check.
@@ -75,8 +76,10 @@ def case_band3d():
 
 
 def case_staged():
-    _gen(P.V1, 36)
-    _gen(P.V1, 128, offset=1)  # misaligned rows: no TMA descriptor
+    # no TMA descriptor when n % 4 != 0 or the rows are not 16-byte aligned
+    _gen(P.V1, 37)
+    _gen(P.V1, 38)
+    _gen(P.V1, 128, offset=1)
     _gen(P.V3, 37)
     _gen(P.V1, 128, env={"CIPRNG_V1_SMEM_STG": "1"}, store_path=P.STORE_DIRECT)
 

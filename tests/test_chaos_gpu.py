@@ -16,11 +16,12 @@ def _i32(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
 
 
+@pytest.mark.parametrize("n_out", [37, 64])  # ragged rows (scalar stores) / 8-word sector chunks
 @pytest.mark.parametrize("n,b,table", [(4, 1, False), (16, 8, False), (32, 3, False), (4, 5, True), (12, 8, True),
-                                       (16, 2, True)])
-def test_alg1_matches_oracle(n, b, table):
+                                       (16, 2, True), (6, 3, False)])
+def test_alg1_matches_oracle(n, b, table, n_out):
     gen = W.rng(700 + n + b)
-    S, n_out = 1000, 37
+    S = 1000
     f = gen.integers(0, 2**n, 2**n).astype(np.uint32) if table else None
     z = gen.integers(1, 2**32, S).astype(np.uint32)
     x = (gen.integers(0, 2**32, S) & ((1 << n) - 1 if n < 32 else 0xFFFFFFFF)).astype(np.uint32)

@@ -151,14 +151,15 @@ def test_v1_generate_host_matches_device():
         assert np.array_equal(dev, host)
 
 
-@pytest.mark.parametrize("variant,n", [(W.V1, 128), (W.V1, 256), (W.V1, 36), (W.V2, 128), (W.V3, 128)])
+@pytest.mark.parametrize("variant,n", [(W.V1, 128), (W.V1, 256), (W.V1, 36), (W.V1, 37), (W.V2, 128), (W.V3, 128)])
 def test_generate_host_multi_chunk(variant, n):
     """prng_generate_host over MORE than one ~64 MiB chunk: the staging double
     buffer with its ev_gen / ev_copy waits, and the store kernels launched
-    with s_begin != 0 into a chunk-sized tensor map -- at least two full chunks
-    + 32 streams, so the last chunk is 32 rows (a multiple of 32, not of 64); n = 256 takes the
-    3-D band kernel, n = 36 the staged path.  Two calls equal prng_generate
-    word for word, and the ragged last group equals the oracle."""
+    with s_begin != 0 into a chunk-sized tensor map -- at least two full
+    chunks + 32 streams, so the last chunk is 32 rows (a multiple of 32, not
+    of 64).  n = 256 takes the 3-D band kernel, n = 36 the 2-D TMA kernel
+    with a partial last box, n = 37 the staged path.  Two calls equal
+    prng_generate word for word, and the ragged last group equals the oracle."""
     rows = (64 << 20) // (4 * n) // 64 * 64   # api.cu prng_generate_host chunk rows
     S = max(2**18, 2 * rows) + 32
     g1 = P.ChaoticPRNG(SEEDS[0], S, variant)
