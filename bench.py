@@ -689,28 +689,58 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
 def measure_c1(P, torch, dev, with_oracle: bool) -> dict:
     """C1 (BASELINE configs[0]): V0 with `paper_defaults` --
     Listing 1 exactly (x = 123123123, Marsaglia's seeds) -- ONE
-    stream, 10^6 outputs in one call.  One GPU thread runs the 10^6 dependent
-    Listing-1 steps (a latency-bound parity config, no roofline).  The oracle
-    (single host core, same workload) is timed beside it and its words
-    compared with the GPU's; the paper ran Listing 1 at 138 MS/s on one Xeon
-    core (P:1040-1041)."""
+    stream, 10^6 outputs per call.  The stream is split over the whole GPU
+    (csrc/v0_jump.cu): GF(2) jump-ahead of Listing 1's three xorshift
+    generators to 128 x 148 segment starts plus an XOR scan of x; the same
+    words as the one-thread chain, which is timed beside it
+    (CIPRNG_V0_JUMP=0).  Calls continue the stream (state carried); the
+    first call builds the jump plan (host polynomials, cached per shape) and
+    is reported separately.  The oracle (single host core, same workload) is
+    timed beside it and its words compared with the GPU's; the paper ran
+    Listing 1 at 138 MS/s on one Xeon core."""
     n = 10**6
     stream = torch.cuda.current_stream()
-    g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
-    out = torch.empty((1, n), dtype=torch.int32, device=dev)
-    g.generate(n, out=out)                       # call 1: the parity call
-    first = P.as_u32(out.cpu()).copy()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3
-    a.record(stream)
-    for _ in range(reps):
-        g.generate(n, out=out)
-    b.record(stream)
-    torch.cuda.synchronize()
-    g.close()
-    s = a.elapsed_time(b) / 1e3 / reps
+
+    def run(env_jump: str, reps: int):
+        old = os.environ.get("CIPRNG_V0_JUMP")
+        os.environ["CIPRNG_V0_JUMP"] = env_jump
+        try:
+            g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
+        finally:
+            if old is None:
+                os.environ.pop("CIPRNG_V0_JUMP", None)
+            else:
+                os.environ["CIPRNG_V0_JUMP"] = old
+        out = torch.empty((1, n), dtype=torch.int32, device=dev)
+        a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a0.record(stream)
+        g.generate(n, out=out)                   # call 1: plan + the parity call
+        b0.record(stream)
+        torch.cuda.synchronize()
+        first_wall = time.perf_counter() - t0
+        first = P.as_u32(out.cpu()).copy()
+        path = int(g.info().store_path)
+        for _ in range(3):
+            g.generate(n, out=out)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            g.generate(n, out=out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        g.close()
+        return a.elapsed_time(b) / 1e3 / reps, a0.elapsed_time(b0), first_wall, first, path
+
+    s, first_ms, first_wall, first, path = run("1", 200)
+    s_seq, _, _, first_seq, _ = run("0", 3)
     row = {"value": n / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": 1, "n": n,
-           "note": "one GPU thread; 10^6 dependent steps (latency-bound parity config)",
+           "path": "jump-ahead (csrc/v0_jump.cu)" if path == 3 else f"store path {path}",
+           "first_call_ms_device": first_ms, "first_call_s_wall_incl_plan": first_wall,
+           "one_thread_chain": {"value": n / s_seq, "ms_per_call": s_seq * 1e3,
+                                "bit_exact_vs_jump": bool(np.array_equal(first, first_seq))},
+           "note": "one V0 stream over the whole GPU: jump-ahead to 128 x 148 segment starts, XOR scan of x; "
+                   "back-to-back calls continue the stream (4 MB of output, L2-resident)",
            "paper_context": {"listing1_one_xeon_core_numbers_per_s": 1.38e8, "source": "PAPER.md P:1040-1041"}}
     if with_oracle:
         import oracle as O

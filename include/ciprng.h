@@ -91,9 +91,14 @@ enum prng_store_path {
     PRNG_STORE_AUTO = 0,   /* TMA tiles when possible, else shared-memory
                               staging + coalesced stores (V1 default tables) */
     PRNG_STORE_DIRECT = 1, /* per-thread 128-bit STG of 4-round buffers   */
-    PRNG_STORE_TMA = 2     /* warp tiles staged in shared memory, written
+    PRNG_STORE_TMA = 2,    /* warp tiles staged in shared memory, written
                               by cp.async.bulk.tensor (V1 default tables,
                               n % 4 == 0); falls back to DIRECT otherwise */
+    PRNG_STORE_JUMP = 3    /* reported by prng_get_info only: a V0 handle
+                              with ONE stream and n >= 4096 splits the
+                              stream over the GPU by GF(2) jump-ahead of
+                              its generators + an XOR scan of x (same
+                              words; BASELINE configs[0] / C1) */
 };
 
 typedef struct prng_config {

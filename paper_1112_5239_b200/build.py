@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libciprng.so")
-SOURCES = ["api.cu", "init_digest.cu", "gen_v0.cu", "gen_v1.cu", "gen_v2.cu", "gen_comb.cu", "bg.cu", "alg1.cu", "emit.cu"]
+SOURCES = ["api.cu", "init_digest.cu", "gen_v0.cu", "gen_v1.cu", "gen_v2.cu", "gen_comb.cu", "bg.cu", "alg1.cu", "emit.cu", "v0_jump.cu"]
 HEADERS = ["device.cuh", "sinks.cuh", "kernels.h", os.path.join("..", "..", "include", "ciprng.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -184,6 +184,9 @@ struct prng_s {
     size_t text_bytes = 0;
     uint8_t *pinned[2] = {nullptr, nullptr};
     size_t pinned_bytes = 0;
+    // V0 single-stream jump-ahead plan (v0_jump.cu); CIPRNG_V0_JUMP=0 disables
+    V0JumpPlan jump;
+    bool jump_on = true;
 };
 
 namespace {
@@ -260,7 +263,11 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
     int launches = 0;
     int path = PRNG_STORE_DIRECT;
     if (h->variant == 0) {
-        launches = launch_v0(a, mode, st);
+        int jl = -1;
+        if (mode == 0 && h->jump_on && h->n_local == 1 && s_count == 1 && n >= kJumpMinN)
+            jl = v0_jump_launch(h->jump, h->state, out, n, st);
+        if (jl > 0) path = PRNG_STORE_JUMP;
+        launches = jl > 0 ? jl : launch_v0(a, mode, st);
     } else if (h->variant == 1) {
         const bool fast = h->default_tables && h->C == 32;
         int kmode = mode;
@@ -403,6 +410,7 @@ int prng_create_shard(uint64_t seed, uint64_t first_stream, uint64_t n_local, in
         if (const char *v = std::getenv(knob); v && v[0]) h->v1tune.shape_set = true;
     if (const char *v = std::getenv("CIPRNG_V2_KIND")) h->v2_kind = std::atoi(v);
     h->v1tune.l2_prefetch = env_on("CIPRNG_V1_PF", false);
+    h->jump_on = env_on("CIPRNG_V0_JUMP", true);
     h->v1tune.smem_stg = env_on("CIPRNG_V1_SMEM_STG", false);
     if (const char *v = std::getenv("CIPRNG_V1_BUFS")) {
         int b = std::atoi(v);
@@ -489,6 +497,7 @@ int prng_destroy(prng_t *h) {
     if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
     cudaFree(h->state);
     cudaFree(h->mod);
+    v0_jump_free(h->jump);
     cudaFree(h->staging[0]);
     cudaFree(h->staging[1]);
     for (int b = 0; b < 2; ++b) {

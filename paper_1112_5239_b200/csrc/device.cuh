@@ -49,18 +49,18 @@ __device__ __forceinline__ uint32_t xor128_f(uint32_t xk, uint32_t wk3) {
     return (wk3 ^ shr_fma<19>(wk3)) ^ (t ^ (t >> 8));
 }
 // Same on 64-bit words (Listing 1's xor128, reading Q2).
-__device__ __forceinline__ uint64_t xor128_f64(uint64_t xk, uint64_t wk3) {
+__host__ __device__ __forceinline__ uint64_t xor128_f64(uint64_t xk, uint64_t wk3) {
     uint64_t t = xk ^ (xk << 11);
     return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
 }
 // xorwow shift register on 64-bit words: v_{k+5} = (v ^ v<<4) ^ (t ^ t<<1),
 // t = x ^ x>>2 with x = v_k, v = v_{k+4} (Q2, Q3).
-__device__ __forceinline__ uint64_t xorwow_f64(uint64_t xk, uint64_t vk4) {
+__host__ __device__ __forceinline__ uint64_t xorwow_f64(uint64_t xk, uint64_t vk4) {
     uint64_t t = xk ^ (xk >> 2);
     return (vk4 ^ (vk4 << 4)) ^ (t ^ (t << 1));
 }
 // Marsaglia xor64 (13, 7, 17) (Listing 1's xorshift, reading Q1-A).
-__device__ __forceinline__ uint64_t xor64_step(uint64_t a) {
+__host__ __device__ __forceinline__ uint64_t xor64_step(uint64_t a) {
     a ^= a << 13;
     a ^= a >> 7;
     a ^= a << 17;

@@ -149,6 +149,25 @@ int launch_alg1(const uint32_t *f, uint32_t n, uint32_t b, uint32_t *z, uint32_t
 int launch_gamma(const uint32_t *f, uint32_t n, uint8_t *mark, unsigned long long *report, cudaStream_t st);
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
                   cudaStream_t st, int grid);
+// v0_jump.cu: one V0 stream split over the GPU by GF(2) jump-ahead + XOR
+// scan (C1).  The plan (jump polynomials for one (L, B)) lives in the handle.
+constexpr int kJumpThreads = 128;  // 256: 34.8 vs 28.8 us per C1 call (more sweeps per SM)
+constexpr int kJumpPolyWords = 6;
+constexpr int kJumpMaxDeg[3] = {64, 256, 320};  // state bits of xor64, xor128-64, xorwow-64
+constexpr uint32_t kJumpMaxL = 64;              // rounds per segment (shared-memory staging)
+constexpr uint64_t kJumpMinN = 4096;            // below this the one-thread chain is as fast
+struct V0JumpPlan {
+    uint64_t *poly = nullptr;   // jump polynomials (v0_jump.cu)
+    uint32_t *flags = nullptr;  // [B] look-back flags, then [B] block aggregates
+    uint32_t L = 0, B = 0, epoch = 0;
+    uint64_t n = 0;    // rounds of the call the launch shape was chosen for
+    size_t smem = 0;
+};
+bool v0_jump_available();
+// >= 1: launches enqueued; < 0: not applicable / failed (caller falls back)
+int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st);
+void v0_jump_free(V0JumpPlan &p);
+
 // emit.cu: format 1 = hex lines (9 B per word), 2 = bit lines (33 B per word)
 int launch_format(const uint32_t *words, uint64_t count, int format, uint8_t *text, cudaStream_t st);
 

@@ -1,0 +1,552 @@
+// v0_jump.cu -- one V0 stream split across the whole GPU (BASELINE configs[0],
+// "1 stream, fixed seed, 10^6 outputs").
+//
+// Listing 1 is one sequential chain per stream: on a GPU a single
+// stream runs on one thread at ~20 M numbers/s (r1's C1 row).  But every
+// generator of Listing 1 is linear over GF(2) -- xor64, xor128 and xorwow's
+// shift register are xorshift recurrences; xorwow's Weyl counter d advances
+// by a constant -- and the chaotic-iteration state is a prefix XOR,
+// x_k = x_0 ^ f_1 ^ ... ^ f_k (Eq. Oplus).  So the stream splits
+// into P = B*T segments of L rounds:
+//
+//  * jump-ahead: with m_g(z) the minimal polynomial of generator g's state
+//    transition A_g (host, once per process: Krylov elimination, verified on
+//    every basis vector), the state J steps ahead is
+//        S_J = sum_i c_i S_i,   c(z) = z^J mod m_g(z),
+//    S_i the state i steps ahead -- a "window" of the generator's own output
+//    sequence.  Two levels: block b jumps from the chunk start with
+//    z^(b T L), thread t from its block's start with z^(t L) (host-computed
+//    polynomials, cached per (L, B) in the handle);
+//  * each thread generates its L words as a LOCAL prefix XOR (staged in
+//    shared memory), a block-wide XOR scan and a look-back over the earlier
+//    blocks' aggregates (cooperative launch: all blocks co-resident) give
+//    every segment its x offset, and the block writes its T*L contiguous
+//    output words coalesced;
+//  * the thread owning the chunk's last round writes the state back.
+//
+// Bit-exact with the sequential chain (and the oracle) by construction: the
+// jump is exact linear algebra over GF(2) and XOR is associative.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels.h"
+
+namespace ciprng {
+
+namespace {
+
+// -------------------------------------------------------------- host GF(2)
+// Polynomials over GF(2): bit i of word i/64 = coefficient of z^i.
+using Poly = std::vector<uint64_t>;
+
+int pdeg(const Poly &p) {
+    for (int w = (int)p.size() - 1; w >= 0; --w)
+        if (p[w]) return 64 * w + 63 - __builtin_clzll(p[w]);
+    return -1;
+}
+inline bool pbit(const Poly &p, int i) { return (p[i >> 6] >> (i & 63)) & 1u; }
+inline void pflip(Poly &p, int i) { p[i >> 6] ^= 1ull << (i & 63); }
+
+// r ^= m << s (m has `words` words, r is long enough)
+void xor_shifted(Poly &r, const Poly &m, int s) {
+    const int ws = s >> 6, bs = s & 63;
+    for (size_t w = 0; w < m.size(); ++w) {
+        if (!m[w]) continue;
+        r[w + ws] ^= m[w] << bs;
+        if (bs && w + ws + 1 < r.size()) r[w + ws + 1] ^= m[w] >> (64 - bs);
+    }
+}
+
+// a * b mod m, deg a, deg b < deg m = dm
+Poly mulmod(const Poly &a, const Poly &b, const Poly &m, int dm) {
+    const size_t W = (size_t)(2 * dm + 64) / 64 + 1;
+    Poly r(W, 0), bb(b);
+    bb.resize(W, 0);
+    for (int i = 0; i <= pdeg(a); ++i)
+        if (pbit(a, i)) xor_shifted(r, b, i);
+    for (int i = pdeg(r); i >= dm; --i)
+        if (pbit(r, i)) xor_shifted(r, m, i - dm);
+    r.resize((size_t)dm / 64 + 1);
+    return r;
+}
+
+// z^e mod m
+Poly zpow(uint64_t e, const Poly &m, int dm) {
+    Poly r((size_t)dm / 64 + 1, 0), base = r;
+    r[0] = 1;  // 1
+    if (dm == 0) return r;
+    base[0] = 2;  // z (dm >= 2 here)
+    while (e) {
+        if (e & 1) r = mulmod(r, base, m, dm);
+        e >>= 1;
+        if (e) base = mulmod(base, base, m, dm);
+    }
+    return r;
+}
+
+// Generator g's state transition on a bit vector of W words.
+void step_state(int g, uint64_t *s) {
+    if (g == 0) {
+        s[0] = xor64_step(s[0]);
+    } else if (g == 1) {
+        const uint64_t nb = xor128_f64(s[0], s[3]);
+        s[0] = s[1]; s[1] = s[2]; s[2] = s[3]; s[3] = nb;
+    } else {
+        const uint64_t nc = xorwow_f64(s[0], s[4]);
+        s[0] = s[1]; s[1] = s[2]; s[2] = s[3]; s[3] = s[4]; s[4] = nc;
+    }
+}
+constexpr int kGenWords[3] = {1, 4, 5};
+
+// Minimal polynomial of the Krylov sequence v, A v, A^2 v, ... by Gaussian
+// elimination: the first A^k v in the span of the earlier ones gives
+// A^k v = sum c_i A^i v, i.e. the polynomial z^k + sum c_i z^i.
+Poly krylov_minpoly(int g, const uint64_t *v0) {
+    const int W = kGenWords[g], D = 64 * W;
+    struct Row {
+        uint64_t v[5];
+        Poly c;
+    };
+    std::vector<int> piv_row(D, -1);
+    std::vector<Row> rows;
+    uint64_t cur[5] = {0, 0, 0, 0, 0};
+    std::memcpy(cur, v0, W * 8);
+    for (int k = 0; k <= D; ++k) {
+        Row r;
+        std::memcpy(r.v, cur, sizeof(r.v));
+        r.c.assign((size_t)D / 64 + 1, 0);
+        pflip(r.c, k);
+        for (int bit = D - 1; bit >= 0; --bit) {
+            if (!((r.v[bit >> 6] >> (bit & 63)) & 1u) || piv_row[bit] < 0) continue;
+            const Row &p = rows[piv_row[bit]];
+            for (int w = 0; w < W; ++w) r.v[w] ^= p.v[w];
+            for (size_t w = 0; w < r.c.size(); ++w) r.c[w] ^= p.c[w];
+        }
+        int top = -1;
+        for (int bit = D - 1; bit >= 0 && top < 0; --bit)
+            if ((r.v[bit >> 6] >> (bit & 63)) & 1u) top = bit;
+        if (top < 0) return r.c;  // dependency found
+        piv_row[top] = (int)rows.size();
+        rows.push_back(r);
+        step_state(g, cur);
+    }
+    return Poly();  // unreachable: D + 1 vectors in a D-dimensional space
+}
+
+// m(A) e_j == 0 for every basis vector e_j
+bool annihilates(int g, const Poly &m) {
+    const int W = kGenWords[g], D = 64 * W, dm = pdeg(m);
+    for (int j = 0; j < D; ++j) {
+        uint64_t cur[5] = {0, 0, 0, 0, 0}, acc[5] = {0, 0, 0, 0, 0};
+        cur[j >> 6] = 1ull << (j & 63);
+        for (int i = 0; i <= dm; ++i) {
+            if (pbit(m, i))
+                for (int w = 0; w < W; ++w) acc[w] ^= cur[w];
+            step_state(g, cur);
+        }
+        for (int w = 0; w < W; ++w)
+            if (acc[w]) return false;
+    }
+    return true;
+}
+
+struct MinPolys {
+    Poly m[3];
+    int deg[3] = {0, 0, 0};
+    bool ok = false;
+};
+
+const MinPolys &min_polys() {
+    static MinPolys mp;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        bool ok = true;
+        for (int g = 0; g < 3; ++g) {
+            // a fixed, dense start vector (SplitMix64 words): a cyclic vector
+            // of A_g with overwhelming probability; verified below
+            uint64_t v[5];
+            for (int w = 0; w < 5; ++w) v[w] = splitmix_fin(0x5EEDull + 0x9E3779B97F4A7C15ull * (uint64_t)(8 * g + w + 1));
+            mp.m[g] = krylov_minpoly(g, v);
+            mp.deg[g] = pdeg(mp.m[g]);
+            ok = ok && mp.deg[g] > 0 && mp.deg[g] <= kJumpMaxDeg[g] && annihilates(g, mp.m[g]);
+        }
+        mp.ok = ok;
+    });
+    return mp;
+}
+
+}  // namespace
+
+bool v0_jump_available() { return min_polys().ok; }
+
+// ------------------------------------------------------------------ kernel
+// Shared-memory windows: generator g's output sequence, window i = state
+// after i steps = words [i, i + kGenWords[g]).  Each array ends in zero
+// words: the padding entries of the jump lists point there.
+constexpr uint32_t kZ1 = kJumpMaxDeg[0], kZ2 = kJumpMaxDeg[1] + 3, kZ3 = kJumpMaxDeg[2] + 4;
+struct JumpSmem {
+    uint64_t w1[kZ1 + 1];
+    uint64_t w2[kZ2 + 4];
+    uint64_t w3[kZ3 + 5];
+    uint64_t part[kJumpThreads / 32][10];
+    uint64_t bstart[10];
+    uint32_t warp_tot[kJumpThreads / 32];
+    uint32_t block_base;
+};
+
+struct JumpArgs {
+    uint32_t *state;        // V0 SoA planes of ONE stream (23 words)
+    uint32_t *out;          // this chunk's first word
+    uint64_t n_chunk;       // rounds in this chunk
+    const uint64_t *poly;   // jump polynomials, generator g at poly + g * (T + B) * kJumpPolyWords:
+                            // thread slots [q][t], then block slots [b][q]
+    uint32_t deg[3];
+    uint32_t L, B;
+    uint32_t *flags;  // [B] epoch flags
+    uint32_t *aggs;   // [B] block aggregates (XOR of the block's f)
+    uint32_t epoch;
+};
+
+// One thread per generator: the first deg_g windows of the state in s10
+// (word layout: a | b0..b3 | c0..c4), then the zero tail.  The register
+// rings are unrolled by their period so the loop body is the recurrence
+// and one shared store per step.
+__device__ __forceinline__ void krylov_windows(JumpSmem &sm, const uint64_t (&s10)[10], const JumpArgs &a) {
+    const uint32_t t = threadIdx.x;
+    if (t == 0) {
+        uint64_t v = s10[0];
+        for (uint32_t i = 0; i < a.deg[0]; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                sm.w1[i + u] = v;
+                v = xor64_step(v);
+            }
+        }
+        sm.w1[kZ1] = 0;
+    } else if (t == 32) {
+        uint64_t b0 = s10[1], b1 = s10[2], b2 = s10[3], b3 = s10[4];
+        sm.w2[0] = b0; sm.w2[1] = b1; sm.w2[2] = b2; sm.w2[3] = b3;
+        for (uint32_t k = 4; k < a.deg[1] + 3; k += 4) {
+            b0 = xor128_f64(b0, b3); sm.w2[k] = b0;
+            b1 = xor128_f64(b1, b0); sm.w2[k + 1] = b1;
+            b2 = xor128_f64(b2, b1); sm.w2[k + 2] = b2;
+            b3 = xor128_f64(b3, b2); sm.w2[k + 3] = b3;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sm.w2[kZ2 + k] = 0;
+    } else if (t == 64) {
+        uint64_t c0 = s10[5], c1 = s10[6], c2 = s10[7], c3 = s10[8], c4 = s10[9];
+        sm.w3[0] = c0; sm.w3[1] = c1; sm.w3[2] = c2; sm.w3[3] = c3; sm.w3[4] = c4;
+        for (uint32_t k = 5; k < a.deg[2] + 4; k += 5) {
+            c0 = xorwow_f64(c0, c4); sm.w3[k] = c0;
+            c1 = xorwow_f64(c1, c0); sm.w3[k + 1] = c1;
+            c2 = xorwow_f64(c2, c1); sm.w3[k + 2] = c2;
+            c3 = xorwow_f64(c3, c2); sm.w3[k + 3] = c3;
+            c4 = xorwow_f64(c4, c3); sm.w3[k + 4] = c4;
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) sm.w3[kZ3 + k] = 0;
+    }
+}
+
+// acc ^= sum over the set bits i of this thread's jump polynomial of window
+// i of w (W words).  Every lane of a warp walks the SAME window index i at
+// the same time -- a broadcast shared load, one wavefront -- and keeps the W
+// words of the window in registers, sliding it by one word per index; the
+// lane's own bit masks the XOR.  (Gathering only the set bits' windows made
+// every load a 32-address gather: ~7 bank-conflicted wavefronts per load,
+// 4x slower.)  The polynomial words of the T thread slots are interleaved
+// ([q][t]) so the warp's poly load is coalesced.
+template <int W, int Q>
+__device__ __forceinline__ void jump_sweep(const uint64_t *w, const uint64_t (&poly)[Q], uint32_t deg, uint64_t *acc) {
+    uint64_t win[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) win[k] = w[k];
+#pragma unroll 1
+    for (uint32_t q = 0; q < (uint32_t)Q && q * 64 < deg; ++q) {
+        uint64_t bits = 0;
+#pragma unroll
+        for (int r = 0; r < Q; ++r)
+            if (r == (int)q) bits = poly[r];
+        const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+#pragma unroll
+        for (uint32_t j = 0; j < 64; ++j) {
+            const uint32_t half = j < 32 ? lo : hi;
+            const uint64_t m = (uint64_t)(int64_t)((int32_t)(half << (31 - (j & 31))) >> 31);
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc[k] ^= win[k] & m;
+#pragma unroll
+            for (int k = 0; k + 1 < W; ++k) win[k] = win[k + 1];
+            win[W - 1] = w[q * 64 + j + W];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
+    extern __shared__ __align__(16) uint8_t jsm_raw[];
+    JumpSmem &sm = *reinterpret_cast<JumpSmem *>(jsm_raw);
+    uint32_t *stage = reinterpret_cast<uint32_t *>(jsm_raw + ((sizeof(JumpSmem) + 15) & ~size_t(15)));
+    const uint32_t T = kJumpThreads, t = threadIdx.x, b = blockIdx.x, L = a.L;
+    const uint32_t lane = t & 31u, warp = t >> 5;
+    const size_t PW = (size_t)(T + a.B) * kJumpPolyWords;  // poly words per generator
+    // this thread's level-2 jump polynomials (z^(t L)), loaded early
+    uint64_t pj1[1], pj2[4], pj3[5];
+    pj1[0] = __ldg(a.poly + t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pj2[q] = __ldg(a.poly + PW + (size_t)q * T + t);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) pj3[q] = __ldg(a.poly + 2 * PW + (size_t)q * T + t);
+
+    // chunk start state (words: a, b0..b3, c0..c4), d, x
+    uint64_t s0[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s0[k] = (uint64_t)a.state[2 * k] | ((uint64_t)a.state[2 * k + 1] << 32);
+    const uint64_t d0 = (uint64_t)a.state[20] | ((uint64_t)a.state[21] << 32);
+    const uint32_t x0 = a.state[22];
+
+    // level 1: this block's start = z^(b T L) applied to the chunk start.
+    // Every thread takes a slice of the list; XOR-reduce over the block.
+    krylov_windows(sm, s0, a);
+    __syncthreads();
+    {
+        uint64_t part[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) part[k] = 0;
+        const size_t boff = (size_t)T * kJumpPolyWords + (size_t)b * kJumpPolyWords;  // block slot b
+        const uint64_t *q1 = a.poly + boff, *q2 = a.poly + PW + boff, *q3 = a.poly + 2 * PW + boff;
+        for (uint32_t i = t; i < a.deg[0]; i += T)
+            if ((q1[i >> 6] >> (i & 63)) & 1u) part[0] ^= sm.w1[i];
+        for (uint32_t i = t; i < a.deg[1]; i += T)
+            if ((q2[i >> 6] >> (i & 63)) & 1u)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) part[1 + k] ^= sm.w2[i + k];
+        for (uint32_t i = t; i < a.deg[2]; i += T)
+            if ((q3[i >> 6] >> (i & 63)) & 1u)
+#pragma unroll
+                for (int k = 0; k < 5; ++k) part[5 + k] ^= sm.w3[i + k];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+#pragma unroll
+            for (int dlt = 16; dlt; dlt >>= 1) part[k] ^= __shfl_xor_sync(kFull, part[k], dlt);
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 10; ++k) sm.part[warp][k] = part[k];
+    }
+    __syncthreads();
+    if (t < 10) {
+        uint64_t v = 0;
+        for (uint32_t w = 0; w < T / 32; ++w) v ^= sm.part[w][t];
+        sm.bstart[t] = v;
+    }
+    __syncthreads();
+    uint64_t sb[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) sb[k] = sm.bstart[k];
+    __syncthreads();
+    // level 2: this thread's start = z^(t L) applied to the block start
+    krylov_windows(sm, sb, a);
+    __syncthreads();
+    uint64_t s[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) s[k] = 0;
+    jump_sweep<1>(sm.w1, pj1, a.deg[0], s);
+    jump_sweep<4>(sm.w2, pj2, a.deg[1], s + 1);
+    jump_sweep<5>(sm.w3, pj3, a.deg[2], s + 5);
+
+    // generate this segment as a local prefix XOR
+    const uint64_t seg = (uint64_t)b * T + t, r0 = seg * L;
+    const uint32_t len = r0 >= a.n_chunk ? 0u : (uint32_t)(a.n_chunk - r0 < L ? a.n_chunk - r0 : L);
+    uint64_t ra = s[0], rb0 = s[1], rb1 = s[2], rb2 = s[3], rb3 = s[4];
+    uint64_t rc0 = s[5], rc1 = s[6], rc2 = s[7], rc3 = s[8], rc4 = s[9];
+    uint64_t rd = d0 + r0 * 362437ull;
+    uint32_t xl = 0;
+    for (uint32_t k = 0; k < len; ++k) {
+        ra = xor64_step(ra);
+        const uint64_t nb = xor128_f64(rb0, rb3);
+        rb0 = rb1; rb1 = rb2; rb2 = rb3; rb3 = nb;
+        const uint64_t nc = xorwow_f64(rc0, rc4);
+        rc0 = rc1; rc1 = rc2; rc2 = rc3; rc3 = rc4; rc4 = nc;
+        rd += 362437u;
+        const uint64_t t3 = rd + nc;
+        xl ^= (uint32_t)ra ^ (uint32_t)(nb >> 32) ^ (uint32_t)(t3 >> 32) ^ (uint32_t)nb ^ (uint32_t)(ra >> 32) ^
+              (uint32_t)t3;
+        stage[t * L + k] = xl;
+    }
+
+    // block-wide exclusive XOR scan of the segment totals
+    uint32_t incl = xl;
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFull, incl, dlt);
+        if (lane >= (uint32_t)dlt) incl ^= v;
+    }
+    if (lane == 31) sm.warp_tot[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, agg = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < T / 32; ++w) {
+        if (w < warp) wpre ^= sm.warp_tot[w];
+        agg ^= sm.warp_tot[w];
+    }
+    const uint32_t excl = wpre ^ incl ^ xl;
+    // publish this block's aggregate, then look back over the earlier blocks
+    // (all co-resident: cooperative launch)
+    if (t == 0) {
+        a.aggs[b] = agg;
+        __threadfence();
+        atomicExch(a.flags + b, a.epoch);
+    }
+    uint32_t prev = 0;
+    for (uint32_t j = t; j < b; j += T) {
+        while (atomicAdd(a.flags + j, 0u) != a.epoch) {
+        }
+        __threadfence();
+        prev ^= *reinterpret_cast<volatile uint32_t *>(a.aggs + j);
+    }
+#pragma unroll
+    for (int dlt = 16; dlt; dlt >>= 1) prev ^= __shfl_xor_sync(kFull, prev, dlt);
+    __syncthreads();  // every warp has read warp_tot above
+    if (lane == 0) sm.warp_tot[warp] = prev;  // reuse: per-warp partial of the look-back
+    __syncthreads();
+    if (t == 0) {
+        uint32_t base = x0;
+        for (uint32_t w = 0; w < T / 32; ++w) base ^= sm.warp_tot[w];
+        sm.block_base = base;
+    }
+    __syncthreads();
+    const uint32_t base = sm.block_base ^ excl;
+    for (uint32_t k = 0; k < len; ++k) stage[t * L + k] ^= base;
+    __syncthreads();
+    // coalesced write of the block's contiguous T*L words
+    const uint64_t blk0 = (uint64_t)b * T * L;
+    const uint64_t blen =
+        blk0 >= a.n_chunk ? 0 : (a.n_chunk - blk0 < (uint64_t)T * L ? a.n_chunk - blk0 : (uint64_t)T * L);
+    for (uint64_t k = t; k < blen; k += T) a.out[blk0 + k] = stage[k];
+
+    // state after the chunk: owned by the segment holding its last round
+    if (len > 0 && r0 + len == a.n_chunk) {
+        const uint64_t v[11] = {ra, rb0, rb1, rb2, rb3, rc0, rc1, rc2, rc3, rc4, rd};
+#pragma unroll
+        for (int k = 0; k < 11; ++k) {
+            a.state[2 * k] = (uint32_t)v[k];
+            a.state[2 * k + 1] = (uint32_t)(v[k] >> 32);
+        }
+        a.state[22] = base ^ xl;
+    }
+}
+
+// ------------------------------------------------------------------- host
+void v0_jump_free(V0JumpPlan &p) {
+    cudaFree(p.poly);
+    cudaFree(p.flags);
+    p = V0JumpPlan();
+}
+
+static size_t jump_smem(uint32_t L) {
+    return ((sizeof(JumpSmem) + 15) & ~size_t(15)) + (size_t)kJumpThreads * L * 4;
+}
+
+// (Re)build the plan for (L, B): polynomials z^(t L), t < T (thread slots,
+// interleaved [q][t]) and z^(b T L), b < B (block slots, [b][q]), as
+// kJumpPolyWords-word bit masks per generator.
+static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t B) {
+    const uint32_t T = kJumpThreads;
+    v0_jump_free(p);
+    const size_t PW = (size_t)(T + B) * kJumpPolyWords;
+    std::vector<uint64_t> host(3 * PW, 0);
+    for (int g = 0; g < 3; ++g) {
+        const int dm = mp.deg[g];
+        const Poly zL = zpow(L, mp.m[g], dm), zTL = zpow((uint64_t)T * L, mp.m[g], dm);
+        for (int level = 0; level < 2; ++level) {
+            const Poly &step = level == 0 ? zL : zTL;
+            const uint32_t n_slots = level == 0 ? T : B;
+            Poly c((size_t)dm / 64 + 1, 0);
+            c[0] = 1;
+            for (uint32_t k = 0; k < n_slots; ++k) {
+                for (size_t q = 0; q < c.size() && q < (size_t)kJumpPolyWords; ++q) {
+                    const size_t pos = level == 0 ? q * T + k : (size_t)T * kJumpPolyWords + (size_t)k * kJumpPolyWords + q;
+                    host[g * PW + pos] = c[q];
+                }
+                c = mulmod(c, step, mp.m[g], dm);
+            }
+        }
+    }
+    if (cudaMalloc(&p.poly, host.size() * 8) != cudaSuccess) return -2;
+    if (cudaMalloc(&p.flags, (size_t)2 * B * 4) != cudaSuccess) return -2;
+    cudaMemcpy(p.poly, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemset(p.flags, 0, (size_t)2 * B * 4);
+    p.L = L;
+    p.B = B;
+    p.epoch = 0;
+    return 0;
+}
+
+int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st) {
+    const MinPolys &mp = min_polys();
+    if (!mp.ok || n == 0) return -1;
+    const uint32_t T = kJumpThreads;
+    // The device queries below cost more host time than the kernel runs, so
+    // they are made once per plan; a call with the plan's n reuses it as is.
+    if (!(p.poly && p.n == n)) {
+        int dev = 0, sms = 148, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // L: about one segment per thread of one CTA per SM, 16..kJumpMaxL rounds
+        uint64_t L = (n + (uint64_t)T * sms - 1) / ((uint64_t)T * sms);
+        L = L < 16 ? 16 : (L > kJumpMaxL ? kJumpMaxL : L);
+        const size_t smem = jump_smem((uint32_t)L);
+        if (cudaFuncSetAttribute(v0_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return -1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v0_jump_kernel, T, smem);
+        if (per_sm < 1) return -1;
+        uint64_t B = (n + T * L - 1) / (T * L);
+        const uint64_t maxB = (uint64_t)sms * (uint64_t)per_sm;
+        if (B > maxB) B = maxB;
+        if (!(p.poly && p.L == L && p.B == B)) {
+            const int rc = v0_jump_build(p, mp, (uint32_t)L, (uint32_t)B);
+            if (rc < 0) return rc;
+        }
+        p.n = n;
+        p.smem = smem;
+    }
+    const uint64_t L = p.L, B = p.B;
+    const size_t smem = p.smem;
+    const uint64_t chunk = (uint64_t)T * B * L;
+    int launches = 0;
+    for (uint64_t r = 0; r < n; r += chunk) {
+        JumpArgs ja;
+        ja.state = state;
+        ja.out = out + r;
+        ja.n_chunk = n - r < chunk ? n - r : chunk;
+        ja.poly = p.poly;
+        for (int g = 0; g < 3; ++g) ja.deg[g] = (uint32_t)mp.deg[g];
+        ja.L = p.L;
+        ja.B = p.B;
+        ja.flags = p.flags;
+        ja.aggs = p.flags + p.B;
+        ja.epoch = ++p.epoch;
+        if (ja.epoch == 0) ja.epoch = ++p.epoch;  // flags start at 0: never reuse 0
+        // cooperative: the look-back spins on earlier blocks' flags
+        const uint32_t blocks = (uint32_t)((ja.n_chunk + (uint64_t)T * L - 1) / ((uint64_t)T * L));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(T);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, v0_jump_kernel, ja) != cudaSuccess) return -3;
+        ++launches;
+    }
+    return launches;
+}
+
+}  // namespace ciprng

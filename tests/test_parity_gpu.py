@@ -233,8 +233,36 @@ def test_v0(seed, S):
 
 
 def test_v0_paper_defaults_c1_full():
-    """BASELINE configs[0]: 1 stream, Listing 1 defaults, 10^6 outputs."""
-    _check(W.V0, 0, 1, [10**6], paper_defaults=True)
+    """BASELINE configs[0]: 1 stream, Listing 1 defaults, 10^6 outputs -- the
+    single-stream jump-ahead path (csrc/v0_jump.cu), checked to be the one
+    that ran."""
+    info = _check(W.V0, 0, 1, [10**6], paper_defaults=True)
+    assert info.store_path == 3, "C1 did not take the jump-ahead path"
+
+
+# one block of T*L rounds is 128*16 = 2048 (n = 4096: 2 blocks); 10^6 + 1
+# leaves a ragged last segment; 3_000_017 > one chunk (128 * 148 * 64 =
+# 1_212_416 rounds on a 148-SM B200): three chunked launches, state carried
+@pytest.mark.parametrize("ns", [[4096, 4097], [5000, 10**6 + 1], [3_000_017, 4099], [4095, 70000, 4096]])
+@pytest.mark.parametrize("seed,paper_defaults", [(0, True), (W.SEEDS[0], False), (W.SEEDS[2], False)])
+def test_v0_single_stream_jump(ns, seed, paper_defaults):
+    """One V0 stream split over the GPU (GF(2) jump-ahead + XOR scan): the
+    same words and end state as the oracle's sequential chain, over several
+    calls (state carried between the jump path and, for n < 4096, the
+    one-thread kernel)."""
+    info = _check(W.V0, seed, 1, ns, paper_defaults=paper_defaults)
+    assert info.store_path == (3 if ns[-1] >= 4096 else 1)
+
+
+def test_v0_jump_equals_sequential_kernel(monkeypatch):
+    """The jump path and the one-thread chain (CIPRNG_V0_JUMP=0) agree word
+    for word at a size the oracle would take seconds on (8 * 10^6)."""
+    n = 8 * 10**6
+    a, pa, ia = gpu_run(W.V0, W.SEEDS[1], 1, [n])
+    monkeypatch.setenv("CIPRNG_V0_JUMP", "0")
+    b, pb, ib = gpu_run(W.V0, W.SEEDS[1], 1, [n])
+    assert ia.store_path == 3 and ib.store_path != 3
+    assert np.array_equal(a[0], b[0]) and np.array_equal(pa, pb)
 
 
 # ------------------------------------------------------------------------ V2

@@ -15,8 +15,8 @@ benchpaths) for sp in 1 2; do timeout 300 python bench.py --store-path $sp --no-
 ref) timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > $O/bench_ref.json 2>> $O/bench.err ;;
 ncu)
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $O/ncu_bench_stdout.txt 2>&1
-  for k in ${NCU_KINDS:-v1 v1direct v2 v0 v3 v4 consume consume_v0 consume_v2 consume_v3 battery cbg alg1}; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:"v1_fast|v2_kernel|v0_kernel|v1_general|comb_|cbg_|alg1_" -s 2 -c 1 -o $O/prof_$k -f python tools/prof_kernels.py $k 4 > $O/ncu_$k.txt 2>&1
+  for k in ${NCU_KINDS:-v1 v1direct v2 v0 v3 v4 consume consume_v0 consume_v2 consume_v3 battery cbg alg1 c1 digest}; do
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:"v1_fast|v2_kernel|v0_kernel|v1_general|comb_|cbg_|alg1_|v0_jump|digest_" -s 2 -c 1 -o $O/prof_$k -f python tools/prof_kernels.py $k 4 > $O/ncu_$k.txt 2>&1
   done ;;
 pipes) timeout 300 python tools/pipe_bench.py > $O/pipes.json 2> $O/pipes.err ;;
 esac

@@ -1,5 +1,5 @@
 """Small driver for ncu captures: a few calls of one workload through the
-C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|v3|v4|consume|consume_v0|consume_v2|consume_v3|battery|cbg|alg1} [calls]"""
+C-ABI.  Usage: python tools/prof_kernels.py {v1|v1direct|v2|v0|v3|v4|consume|consume_v0|consume_v2|consume_v3|battery|cbg|alg1|c1|digest} [calls]"""
 import os
 import sys
 
@@ -61,6 +61,19 @@ elif which == "alg1":
     x = torch.zeros(2**20, dtype=torch.int32, device="cuda")
     for _ in range(calls):
         CH.alg1_generate(32, 8, z, x, 64)
+elif which == "c1":
+    n = 10**6
+    g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
+    out = torch.empty((1, n), dtype=torch.int32, device="cuda")
+    for _ in range(calls):
+        g.generate(n, out=out)
+elif which == "digest":
+    S, n = 2**23, 256
+    out = torch.empty((S, n), dtype=torch.int32, device="cuda")
+    g = P.ChaoticPRNG(seed, S, P.V1)
+    g.generate(n, out=out)
+    for _ in range(calls):
+        P.digest(out)
 elif which in ("consume", "consume_v0", "consume_v2", "consume_v3"):
     S, n = 2**20, 1024
     var = {"consume": P.V1, "consume_v0": P.V0, "consume_v2": P.V2, "consume_v3": P.V3}[which]
