@@ -122,7 +122,9 @@ def pipe_roofline(rate: float, cap: dict, numbers: int, src: str) -> dict:
 
     ncu gives, for one launch of `numbers` numbers, the busy fraction of the
     ALU and heavy-FMA pipes (sm__pipe_{alu,fmaheavy}_cycles_active, % of peak
-    sustained over the elapsed cycles).  Busy pipe-cycles per number =
+    sustained over the elapsed cycles) and of the L1/shared-memory data pipe
+    (l1tex__data_pipe_lsu_wavefronts: the consumers' histogram atomics); the
+    busiest of the three is the binding one.  Busy pipe-cycles per number =
     fraction x duration x SM clock x 148 SMs / numbers; `achieved` = that x
     the live bench rate, `peak` = 148 SMs x the max SM clock (the pipe busy
     every cycle on every SM), so `frac` is the live rate's busy fraction of
@@ -130,15 +132,19 @@ def pipe_roofline(rate: float, cap: dict, numbers: int, src: str) -> dict:
     over the 4-scheduler issue peak) is reported beside it."""
     alu = cap.get("pipe_alu_cycles_pct", 0.0) / 100.0
     heavy = cap.get("pipe_fmaheavy_cycles_pct", 0.0) / 100.0
-    pipe, busy = ("fmaheavy", heavy) if heavy > alu else ("alu", alu)
+    # the L1/shared data pipe (one wavefront per SM per cycle): the consumers'
+    # bank-conflicted histogram atomics load it as much as the ALU
+    lsu = cap.get("lsu_data_pct", 0.0) / 100.0
+    pipe, busy = max((("alu", alu), ("fmaheavy", heavy), ("lsu_data", lsu)), key=lambda kv: kv[1])
     cyc_per_number = busy * cap["duration"] * cap["sm_clock"] * N_SM / numbers
     peak = N_SM * SM_MAX_HZ
     ach = rate * cyc_per_number
     ipn = cap["warp_insts"] * 32 / numbers
     return {"bound": pipe, "achieved": ach / 1e12, "peak": peak / 1e12, "unit": "T pipe-cycles/s",
             "frac": ach / peak, "pipe_cycles_per_number": cyc_per_number,
-            "ncu_busy_frac": {"alu": alu, "fmaheavy": heavy}, "kernel": cap.get("kernel"),
-            "source": f"{src} (ncu --set full: sm__pipe_*_cycles_active, gpu__time_duration, "
+            "ncu_busy_frac": {"alu": alu, "fmaheavy": heavy, "lsu_data": lsu}, "kernel": cap.get("kernel"),
+            "source": f"{src} (ncu --set full: sm__pipe_*_cycles_active, l1tex__data_pipe_lsu_wavefronts, "
+                      "gpu__time_duration, "
                       "sm__cycles_elapsed.avg.per_second); peak = 148 SMs x 1.965 GHz",
             "issue": {"inst_per_number": ipn, "achieved": rate * ipn / 1e12, "peak": ISSUE_PEAK_TLANE,
                       "unit": "T lane-inst/s", "frac": rate * ipn / 1e12 / ISSUE_PEAK_TLANE}}

@@ -33,6 +33,8 @@ METRICS = [
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "pipe_lsu_pct"),
     ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "pipe_fmaheavy_cycles_pct"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "pipe_alu_cycles_pct"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "lsu_data_pct"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum", "smem_atom_conflicts"),
     ("smsp__inst_executed.sum", "warp_insts"),
     ("lts__t_sectors_srcunit_tex_op_write.sum", "l2_write_sectors"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall_long_sb"),
