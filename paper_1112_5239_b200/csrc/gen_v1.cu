@@ -118,7 +118,8 @@ constexpr int v1_fast_min_blocks() {
 #endif
 template <class Sink>
 constexpr int v1_fast_max_threads() {
-    return std::is_same<Sink, StatsSink>::value ? CIPRNG_EXP_V1C_THREADS : 256;
+    return (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkLane>::value) ? CIPRNG_EXP_V1C_THREADS
+                                                                                              : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int v1_fast_min_blocks_x() {
@@ -520,9 +521,19 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
                 const size_t sm = 4 * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
             } else {
+#if defined(CIPRNG_V1_HIST_PRIV)
+                // experiment: per-lane private histogram columns (sinks.cuh StatsSinkLane)
+                constexpr int kW = CIPRNG_V1_HIST_PRIV;  // warps per CTA
+                auto kern = v1_fast_kernel<StatsSinkLane, 0>;
+                const size_t sm = kW * StatsSinkLane::kSmemBytesPerWarp + StatsSinkLane::kSmemBytesExtra;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                const uint64_t needw = (tiles + kW - 1) / kW;
+                launch_k(kern, dim3(persistent_grid(kern, 32 * kW, sm, needw)), dim3(32 * kW), sm, st, a, *tmap);
+#else
                 auto kern = v1_fast_kernel<StatsSink, 0>;
                 const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);
+#endif
             }
         }
     } else {

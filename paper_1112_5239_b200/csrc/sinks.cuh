@@ -248,6 +248,122 @@ struct StatsSink {
     static constexpr bool kStats = true;
 };
 
+// StatsSink with a PRIVATE histogram column per lane (experiment
+// CIPRNG_V1_HIST_PRIV, V1 fast consumer only).  The shared histogram's random
+// bins cost ~3.15 bank-conflicted wavefronts per ATOMS (ncu r2a: the
+// L1/shared data pipe 72 % busy).  Here bin b of lane l is the 16-bit half
+// (l & 1) of word b*16 + (l >> 1): lanes 2k, 2k+1 share bank k + 16 (b & 1),
+// so an atomic is at most 2-way conflicted.  16 KiB per warp (fewer
+// resident warps); the u16 halves are folded into u64 before they could
+// carry into the neighbour half.  Measured (C5 shape, L2 flushed, parity
+// green, profiles/experiments/s52_hist_priv.jsonl): 1.70e12 numbers/s at 1,
+// 2 or 4 warps per CTA against 1.82e12 for the shared histogram -- the
+// occupancy lost to 16 KiB per warp (<= 14 warps/SM vs 24) costs more than
+// the bank conflicts saved.  Kept as the measured alternative, off.
+struct StatsSinkLane {
+    uint32_t col;        // shared address of this lane's column: warp base + (lane >> 1) * 4
+    uint32_t inc;        // 1 (even lane) or 65536 (odd lane)
+    uint32_t warp_base;  // shared address of the warp's 4096 words
+    uint32_t cta_bins;   // shared address of the CTA's u64 bins[256]
+    uint32_t out32;
+    uint64_t outside, pairs;
+    uint32_t pend[2];
+    uint64_t n;
+    uint64_t pending;  // increments of one lane's bin since the last fold (upper bound)
+    static constexpr int kWordsPerWarp = 4096;
+    __device__ __forceinline__ explicit StatsSinkLane(const GenArgs &a)
+        : out32(0), outside(0), pairs(0), pend{0, 0}, n(a.n), pending(0) {
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+        const uint32_t all = smem_u32(smem_dyn);
+        cta_bins = all;  // 2 KiB of u64 bins first
+        warp_base = all + 2048u + warp * (kWordsPerWarp * 4u);
+        col = warp_base + (lane >> 1) * 4u;
+        inc = (lane & 1u) ? 65536u : 1u;
+        for (uint32_t k = lane; k < (uint32_t)kWordsPerWarp / 4u; k += 32u)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(warp_base + 16u * k), "r"(0u) : "memory");
+        uint64_t *cb = reinterpret_cast<uint64_t *>(smem_dyn);
+        for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) cb[b] = 0;
+        __syncthreads();
+    }
+    __device__ __forceinline__ void bin(uint32_t add, uint32_t o) {
+        asm volatile("{\n\t.reg .u32 b, a;\n\tshr.u32 b, %0, 24;\n\tmad.lo.u32 a, b, 64, %1;\n\t"
+                     "red.shared.add.u32 [a], %2;\n\t}" ::"r"(o), "r"(col), "r"(add) : "memory");
+    }
+    __device__ __forceinline__ void pair(uint32_t u, uint32_t v) { count_outside(out32, u, v); }
+    __device__ __forceinline__ void begin_row(int, uint64_t) {}
+    __device__ __forceinline__ void put4(int, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
+                                         bool valid) {
+        const uint32_t add = valid ? inc : 0u;
+        bin(add, o0);
+        bin(add, o1);
+        bin(add, o2);
+        bin(add, o3);
+        pair(o0, o1);
+        pair(o2, o3);
+    }
+    __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
+        bin(valid ? inc : 0u, o);
+        if (i & 1) pair(pend[slot], o);
+        else pend[slot] = o;
+    }
+    // fold the warp's 16 lane-pair columns into the CTA's u64 bins and zero
+    // them (all 32 lanes together): lane l sums bins l, l + 32, ...
+    __device__ __forceinline__ void fold() {
+        __syncwarp();
+        const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll 1
+        for (uint32_t b = lane; b < 256u; b += 32u) {
+            uint32_t lo = 0, hi = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < 16u; k += 4u) {
+                uint32_t v0, v1, v2, v3;
+                const uint32_t addr = warp_base + (b * 16u + k) * 4u;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                             : "r"(addr));
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0u) : "memory");
+                lo += (v0 & 0xFFFFu) + (v1 & 0xFFFFu) + (v2 & 0xFFFFu) + (v3 & 0xFFFFu);
+                hi += (v0 >> 16) + (v1 >> 16) + (v2 >> 16) + (v3 >> 16);
+            }
+            const uint64_t tot = (uint64_t)lo + hi;
+            if (tot) asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(cta_bins + 8u * b), "l"(tot) : "memory");
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ void end_rows(uint32_t rows) {
+        outside += rows ? out32 : 0u;
+        out32 = 0;
+        pairs += (uint64_t)rows * (n >> 1);
+        pending += 2 * n;                  // a lane adds at most 2 per round to one bin
+        if (pending + 2 * n >= 65536u) {  // warp-uniform
+            fold();
+            pending = 0;
+        }
+    }
+    __device__ void finish(const GenArgs &a) {
+        uint64_t v = pairs - outside, p = pairs;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            v += __shfl_xor_sync(kFull, v, d);
+            p += __shfl_xor_sync(kFull, p, d);
+        }
+        fold();
+        __syncthreads();
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        const uint64_t *cb = reinterpret_cast<const uint64_t *>(smem_dyn);
+        for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x)
+            if (cb[b]) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 2 + b), (unsigned long long)cb[b]);
+        if ((threadIdx.x & 31) == 0) {
+            if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 0), (unsigned long long)v);
+            if (p) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 1), (unsigned long long)p);
+        }
+    }
+    static constexpr int kSmemBytesPerWarp = kWordsPerWarp * 4;
+    static constexpr int kSmemBytesExtra = 2048;
+    static constexpr bool kStats = true;
+};
+
 // Statistical battery counts (reading
 // Q31: a stream's bit sequence within one call is its words in round order,
 // each most significant bit first).  Same state evolution as StatsSink; per
