@@ -360,6 +360,14 @@ CIPRNG_API int prng_selftest_modsq(uint64_t *mismatches);
  * no GPU), PRNG_EINVAL for a null pointer. */
 CIPRNG_API int prng_selftest_modsq_gpu(uint64_t *mismatches);
 
+/* Host-only self-test of the single-stream jump-ahead (PRNG_STORE_JUMP): the
+ * minimal polynomials of Listing 1's three generators (xor64, xor128 and
+ * xorwow on 64-bit words) and, from seeded states, the state J
+ * steps ahead as sum_i c_i S_i (c = z^J mod m) against J plain steps.
+ * *mismatches = 0 when every check holds; degrees[3] = the three minimal
+ * polynomials' degrees.  No GPU needed. */
+CIPRNG_API int prng_selftest_jump(uint64_t *mismatches, uint32_t *degrees);
+
 /* Library build string (compiler, arch). */
 CIPRNG_API const char *prng_version(void);
 

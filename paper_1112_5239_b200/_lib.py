@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
             "prng_last_cuda_error": ([], ctypes.c_char_p),
             "prng_selftest_modsq": ([ctypes.POINTER(u64)], i32),
             "prng_selftest_modsq_gpu": ([ctypes.POINTER(u64)], i32),
+            "prng_selftest_jump": ([ctypes.POINTER(u64), ctypes.POINTER(u32)], i32),
             "prng_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():

@@ -869,6 +869,11 @@ int prng_selftest_modsq(uint64_t *mismatches) {
     return PRNG_OK;
 }
 
+int prng_selftest_jump(uint64_t *mismatches, uint32_t *degrees) {
+    if (!mismatches || !degrees) return PRNG_EINVAL;
+    return v0_jump_selftest(mismatches, degrees);
+}
+
 int prng_selftest_modsq_gpu(uint64_t *mismatches) {
     if (!mismatches) return PRNG_EINVAL;
     std::vector<uint32_t> tab = modulus_table();

@@ -164,6 +164,7 @@ struct V0JumpPlan {
     size_t smem = 0;
 };
 bool v0_jump_available();
+int v0_jump_selftest(uint64_t *mismatches, uint32_t *degrees);  // host only
 // >= 1: launches enqueued; < 0: not applicable / failed (caller falls back)
 int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st);
 void v0_jump_free(V0JumpPlan &p);

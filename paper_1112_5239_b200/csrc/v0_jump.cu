@@ -182,6 +182,44 @@ const MinPolys &min_polys() {
 
 bool v0_jump_available() { return min_polys().ok; }
 
+// Host self-test of the jump-ahead algebra (no GPU): for each generator, from
+// a few seeded states, the state J steps ahead computed as sum_i c_i S_i with
+// c = z^J mod m_g must equal J plain steps, for J up to 3*10^5.
+int v0_jump_selftest(uint64_t *mismatches, uint32_t *degrees) {
+    const MinPolys &mp = min_polys();
+    uint64_t bad = mp.ok ? 0 : 1;
+    for (int g = 0; g < 3; ++g) {
+        degrees[g] = (uint32_t)mp.deg[g];
+        if (!mp.ok) continue;
+        const int W = kGenWords[g], dm = mp.deg[g];
+        for (uint64_t seed = 1; seed <= 3; ++seed) {
+            uint64_t s[5];
+            for (int w = 0; w < 5; ++w) s[w] = splitmix_fin(seed * 0x9E3779B97F4A7C15ull + 77u * (uint64_t)(w + 1) + g);
+            std::vector<uint64_t> win((size_t)dm * W);
+            uint64_t cur[5];
+            std::memcpy(cur, s, sizeof(cur));
+            for (int i = 0; i < dm; ++i) {
+                std::memcpy(&win[(size_t)i * W], cur, (size_t)W * 8);
+                step_state(g, cur);
+            }
+            uint64_t ref[5];
+            std::memcpy(ref, s, sizeof(ref));
+            uint64_t done = 0;
+            for (uint64_t J : {0ull, 1ull, 2ull, 63ull, 64ull, 253ull, 320ull, 1000ull, 6784ull, 299999ull}) {
+                for (; done < J; ++done) step_state(g, ref);
+                const Poly c = zpow(J, mp.m[g], dm);
+                uint64_t acc[5] = {0, 0, 0, 0, 0};
+                for (int i = 0; i < dm; ++i)
+                    if (pbit(c, i))
+                        for (int w = 0; w < W; ++w) acc[w] ^= win[(size_t)i * W + w];
+                for (int w = 0; w < W; ++w) bad += acc[w] != ref[w];
+            }
+        }
+    }
+    *mismatches = bad;
+    return 0;
+}
+
 // ------------------------------------------------------------------ kernel
 // Shared-memory windows: generator g's output sequence, window i = state
 // after i steps = words [i, i + kGenWords[g]).  Each array ends in zero

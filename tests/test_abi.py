@@ -38,6 +38,20 @@ def test_barrett_modsq_exhaustive():
     assert bad.value == 0
 
 
+def test_jump_ahead_selftest():
+    """C1's single-stream split (csrc/v0_jump.cu): the host minimal
+    polynomials of Listing 1's generators annihilate every basis vector, and
+    jumps of J in {0 .. 299999} steps equal J plain steps from seeded states.
+    xor64 and xorwow on 64-bit words have full-degree minimal polynomials
+    (64, 320); Listing 1's xor128 on 64-bit words (shifts 11, 19, 8) has
+    degree 253 < 256."""
+    bad = ctypes.c_uint64(123)
+    deg = (ctypes.c_uint32 * 3)()
+    assert P.lib().prng_selftest_jump(ctypes.byref(bad), deg) == 0
+    assert bad.value == 0
+    assert list(deg) == [64, 253, 320]
+
+
 def _create(seed, first, n_local, variant, comb_size=0, comb=None, paper_defaults=0, store_path=0):
     keep = None
     if comb is not None:
@@ -112,6 +126,7 @@ def test_python_binding_mirrors_abi_names():
     """The binding exposes every C-ABI entry point that takes work under its
     own name (marshalling only; no compute on import)."""
     compute = [s for s in P.declared_symbols() if s not in (
-        "prng_strerror", "prng_last_cuda_error", "prng_selftest_modsq", "prng_selftest_modsq_gpu", "prng_version")]
+        "prng_strerror", "prng_last_cuda_error", "prng_selftest_modsq", "prng_selftest_modsq_gpu", "prng_selftest_jump",
+        "prng_version")]
     missing = [s for s in compute if not callable(getattr(P, s, None))]
     assert not missing, missing
