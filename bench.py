@@ -891,7 +891,6 @@ def measure_secondary(P, torch, dev, args):
             res[name]["heavy_fma_model"] = {"peak_squarings_per_s": sq_peak, "frac": 12 * S5 * n5 / s / sq_peak}
         g.close()
     res["c5_consume_allreduce"] = measure_c5_sharded(P, torch, dev, timed)
-    res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
     from paper_1112_5239_b200 import battery as B
 
     g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
@@ -930,6 +929,9 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: CH.alg1_generate(32, 8, za, xa, na), 10)
     res["alg1_negation_b8"] = {"value": Sa * na / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": Sa,
                                "n": na, "cells": 32, "b": 8}
+    # last: the 10^12-number job runs the GPU hot for seconds (power cap),
+    # which slowed the row measured right after it by up to 13 % (r2b battery)
+    res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
     return res
 
 

@@ -165,7 +165,9 @@ struct V0JumpPlan {
 };
 bool v0_jump_available();
 int v0_jump_selftest(uint64_t *mismatches, uint32_t *degrees);  // host only
-// >= 1: launches enqueued; < 0: not applicable / failed (caller falls back)
+// >= 1: launches enqueued; -1..-3: not applicable / nothing enqueued (the
+// caller falls back to the one-thread kernel); -4: a later chunk failed to
+// launch after earlier chunks ran (the call fails, PRNG_ECUDA)
 int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st);
 void v0_jump_free(V0JumpPlan &p);
 

@@ -581,7 +581,16 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
         at[0].val.cooperative = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, v0_jump_kernel, ja) != cudaSuccess) return -3;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, v0_jump_kernel, ja);
+        if (e != cudaSuccess) {
+            // nothing enqueued yet: the caller may fall back to the one-thread
+            // kernel; after a chunk ran, the state has moved -- report it
+            if (launches == 0) {
+                cudaGetLastError();  // clear the launch error before the fallback
+                return -3;
+            }
+            return -4;
+        }
         ++launches;
     }
     return launches;
