@@ -27,6 +27,7 @@
 // Bit-exact with the sequential chain (and the oracle) by construction: the
 // jump is exact linear algebra over GF(2) and XOR is associative.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -246,7 +247,30 @@ struct JumpArgs {
     uint32_t *flags;  // [B] epoch flags
     uint32_t *aggs;   // [B] block aggregates (XOR of the block's f)
     uint32_t epoch;
+    unsigned long long *dbg;  // CIPRNG_JUMP_TIMING builds: [B][16] phase timestamps
 };
+
+// Phase timestamps (diagnostic builds, -DCIPRNG_JUMP_TIMING): thread 0 of
+// every CTA records %globaltimer at each phase boundary; the host prints the
+// latest CTA's time per phase.  Measured (r2, 10^6 numbers, 28 us): Krylov
+// windows 2.0, block jump 4.3, Krylov again 1.6, thread sweeps 13.3,
+// generation 2.7, scans + look-back 3.4, write 0.5 us -- the sweeps are ALU
+// bound (math-throttle and barrier stalls; splitting each segment's sweep
+// over 4 threads did not help, 30.7 us).
+#if defined(CIPRNG_JUMP_TIMING)
+#define JT(k)                                                              \
+    do {                                                                   \
+        if (t == 0 && a.dbg) {                                             \
+            unsigned long long ts;                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));         \
+            a.dbg[b * 16 + (k)] = ts;                                      \
+        }                                                                  \
+    } while (0)
+#else
+#define JT(k) \
+    do {      \
+    } while (0)
+#endif
 
 // One thread per generator: the first deg_g windows of the state in s10
 // (word layout: a | b0..b3 | c0..c4), then the zero tail.  The register
@@ -347,8 +371,10 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
 
     // level 1: this block's start = z^(b T L) applied to the chunk start.
     // Every thread takes a slice of the list; XOR-reduce over the block.
+    JT(0);
     krylov_windows(sm, s0, a);
     __syncthreads();
+    JT(1);
     {
         uint64_t part[10];
 #pragma unroll
@@ -386,8 +412,10 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     for (int k = 0; k < 10; ++k) sb[k] = sm.bstart[k];
     __syncthreads();
     // level 2: this thread's start = z^(t L) applied to the block start
+    JT(2);
     krylov_windows(sm, sb, a);
     __syncthreads();
+    JT(3);
     uint64_t s[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) s[k] = 0;
@@ -395,6 +423,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     jump_sweep<4>(sm.w2, pj2, a.deg[1], s + 1);
     jump_sweep<5>(sm.w3, pj3, a.deg[2], s + 5);
 
+    JT(4);
     // generate this segment as a local prefix XOR
     const uint64_t seg = (uint64_t)b * T + t, r0 = seg * L;
     const uint32_t len = r0 >= a.n_chunk ? 0u : (uint32_t)(a.n_chunk - r0 < L ? a.n_chunk - r0 : L);
@@ -415,6 +444,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
         stage[t * L + k] = xl;
     }
 
+    JT(5);
     // block-wide exclusive XOR scan of the segment totals
     uint32_t incl = xl;
 #pragma unroll
@@ -431,6 +461,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
         agg ^= sm.warp_tot[w];
     }
     const uint32_t excl = wpre ^ incl ^ xl;
+    JT(6);
     // publish this block's aggregate, then look back over the earlier blocks
     // (all co-resident: cooperative launch)
     if (t == 0) {
@@ -459,12 +490,14 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     const uint32_t base = sm.block_base ^ excl;
     for (uint32_t k = 0; k < len; ++k) stage[t * L + k] ^= base;
     __syncthreads();
+    JT(7);
     // coalesced write of the block's contiguous T*L words
     const uint64_t blk0 = (uint64_t)b * T * L;
     const uint64_t blen =
         blk0 >= a.n_chunk ? 0 : (a.n_chunk - blk0 < (uint64_t)T * L ? a.n_chunk - blk0 : (uint64_t)T * L);
     for (uint64_t k = t; k < blen; k += T) a.out[blk0 + k] = stage[k];
 
+    JT(8);
     // state after the chunk: owned by the segment holding its last round
     if (len > 0 && r0 + len == a.n_chunk) {
         const uint64_t v[11] = {ra, rb0, rb1, rb2, rb3, rc0, rc1, rc2, rc3, rc4, rd};
@@ -567,6 +600,13 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
         ja.B = p.B;
         ja.flags = p.flags;
         ja.aggs = p.flags + p.B;
+        ja.dbg = nullptr;
+#if defined(CIPRNG_JUMP_TIMING)
+        static unsigned long long *dbg = nullptr;
+        if (!dbg) cudaMalloc(&dbg, (size_t)16 * 4096 * 8);
+        cudaMemset(dbg, 0, (size_t)16 * 4096 * 8);
+        ja.dbg = dbg;
+#endif
         ja.epoch = ++p.epoch;
         if (ja.epoch == 0) ja.epoch = ++p.epoch;  // flags start at 0: never reuse 0
         // cooperative: the look-back spins on earlier blocks' flags
@@ -592,6 +632,20 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
             return -4;
         }
         ++launches;
+#if defined(CIPRNG_JUMP_TIMING)
+        {
+            std::vector<unsigned long long> h((size_t)16 * blocks);
+            cudaMemcpy(h.data(), ja.dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+            unsigned long long t0 = ~0ull;
+            for (uint32_t bb = 0; bb < blocks; ++bb) t0 = std::min(t0, h[bb * 16]);
+            double mx[9] = {0};
+            for (uint32_t bb = 0; bb < blocks; ++bb)
+                for (int k = 0; k < 9; ++k) mx[k] = std::max(mx[k], (double)(h[bb * 16 + k] - t0) * 1e-3);
+            fprintf(stderr, "jump phases (us, latest CTA, from the first start): start %.2f krylov1 %.2f lvl1 %.2f "
+                    "krylov2 %.2f sweep %.2f gen %.2f scan %.2f lookback %.2f write %.2f\n",
+                    mx[0], mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7], mx[8]);
+        }
+#endif
     }
     return launches;
 }
