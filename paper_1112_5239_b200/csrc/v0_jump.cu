@@ -252,11 +252,11 @@ struct JumpArgs {
 
 // Phase timestamps (diagnostic builds, -DCIPRNG_JUMP_TIMING): thread 0 of
 // every CTA records %globaltimer at each phase boundary; the host prints the
-// latest CTA's time per phase.  Measured (r2, 10^6 numbers, 28 us): Krylov
-// windows 2.0, block jump 4.3, Krylov again 1.6, thread sweeps 13.3,
-// generation 2.7, scans + look-back 3.4, write 0.5 us -- the sweeps are ALU
-// bound (math-throttle and barrier stalls; splitting each segment's sweep
-// over 4 threads did not help, 30.7 us).
+// latest CTA's time per phase.  Measured (r2, 10^6 numbers, 27 us): Krylov
+// windows 1.9, block jump 4.5, Krylov again 1.6, thread sweeps 11.8,
+// generation 2.7, scans + look-back 3.6, write 0.5 us -- the sweeps are ALU
+// bound (math-throttle stalls; splitting each segment's sweep over 4 threads
+// did not help, 30.7 us per call).
 #if defined(CIPRNG_JUMP_TIMING)
 #define JT(k)                                                              \
     do {                                                                   \
