@@ -13,6 +13,7 @@ Store paths covered (csrc/api.cu run_pass):
   * 3-D band boxes (V1 n = 256)
   * staged shared-memory + coalesced STG (V1 / V3 n % 4 != 0; misaligned output)
   * direct 128-bit / scalar stores (STORE_DIRECT; V0, V2, V4)
+  * the single-stream V0 jump-ahead kernel (C1)
 plus the fused consumer (V0..V4), the battery, generate_host, the digest,
 chaotic Blum-Goldwasser encrypt / decrypt, Algorithm 1 and the Gamma(f) check.
 
@@ -90,6 +91,19 @@ def case_direct():
     _gen(P.V2, 17)
 
 
+def case_jump():
+    # one V0 stream split over the GPU (csrc/v0_jump.cu: shared-memory windows,
+    # block scans, cooperative look-back); 3 CTAs of 128 segments x 16 rounds
+    for n in (5000, 4096):
+        _gen(P.V0, n, S_=1)
+    g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
+    st = O.init_states(P.V0, 0, 0, 1, paper_defaults=True)
+    got = P.as_u32(g.generate(6000))
+    assert np.array_equal(got, O.generate(P.V0, st, 6000)), "jump paper_defaults"
+    assert int(g.info().store_path) == 3, "jump path not taken"
+    g.close()
+
+
 def case_consume():
     for v, n in ((P.V0, 20), (P.V1, 64), (P.V1, 66), (P.V2, 16), (P.V3, 64), (P.V4, 20)):
         g = P.ChaoticPRNG(SEED, S, v)
@@ -120,7 +134,10 @@ def case_digest():
     # direct stores: initcheck does not see TMA (async-proxy) writes
     g = P.ChaoticPRNG(SEED, S, P.V1, store_path=P.STORE_DIRECT)
     out = g.generate(64)
-    d = int(P.as_u64(P.digest(out, 5))[0])
+    # accumulator initialised by a host copy (initcheck tracks copies; a torch
+    # fill kernel is outside the --kernel-name filter and would not count)
+    acc = torch.tensor([0], dtype=torch.int64, device="cuda")
+    d = int(P.as_u64(P.digest(out, 5, acc))[0])
     ref = int(O.digest(P.as_u32(out), 5))
     assert d == ref, "digest"
     g.close()

@@ -114,3 +114,16 @@ def test_emit_cli_to_stdout():
     st = O.init_states(W.V1, SEED, 0, 64)
     ref = np.concatenate([O.generate(W.V1, st, 8).reshape(-1) for _ in range(2)])
     assert r.stdout == ref.astype("<u4").tobytes()
+
+
+def test_emit_single_stream_jump_path(tmp_path):
+    """prng_emit over the C1 jump-ahead path (one V0 stream, n >= 4096): the
+    hex lines equal the oracle's sequential chain."""
+    n = 5000
+    g = P.ChaoticPRNG(SEED, 1, W.V0)
+    path = tmp_path / "j.txt"
+    assert g.emit(n, str(path), "hex") == 9 * n
+    assert int(g.info().store_path) == 3
+    ref = O.generate(W.V0, O.init_states(W.V0, SEED, 0, 1), n)
+    assert path.read_bytes() == _serialise(ref, "hex")
+    g.close()

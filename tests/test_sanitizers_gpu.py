@@ -19,14 +19,14 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-CASES = ["tma2d", "band3d", "staged", "direct", "consume", "battery", "host", "digest", "bg", "chaos"]
+CASES = ["tma2d", "band3d", "staged", "direct", "jump", "consume", "battery", "host", "digest", "bg", "chaos"]
 # initcheck does not see writes made by the async proxy (cp.async.bulk.tensor
 # stores): every word a TMA-path kernel wrote is reported as uninitialised
 # when it is copied back, although each case checks every word against the
 # oracle (gpurun_out/sanitizer_initcheck.log of r2: 94064 reports, all
 # "cudaMemcpy source", all on TMA-written buffers).  initcheck therefore
 # runs the cases whose stores are ordinary STG.
-INITCHECK_CASES = ["staged", "direct", "consume", "battery", "digest", "bg", "chaos"]
+INITCHECK_CASES = ["staged", "direct", "jump", "consume", "battery", "digest", "bg", "chaos"]
 
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
