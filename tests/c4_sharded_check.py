@@ -1,7 +1,7 @@
 """BASELINE configs[3]: stream-sharded generation of ~10^12 numbers, output
 identical at every GPU count.
 
-  python tools/c4_sharded.py [--calls 466] [--gpus-simulated 1,2,4,8] [--verify-groups 64]
+  python tests/c4_sharded_check.py [--calls 466] [--gpus-simulated 1,2,4,8] [--verify-groups 64]
 
 V1, 2^23 streams x 256 numbers per call, 466 calls = 1,000,727,379,968
 numbers.  For each shard count G the stream space is split with

@@ -3,4 +3,4 @@
 TAG=${1:-r1j}
 bash tools/gpu_session.sh $TAG smoke tests bench ref ncu
 O=gpurun_out/$TAG
-timeout 900 python tools/c4_sharded.py > $O/c4_sharded.json 2> $O/c4_sharded.err; echo rc=$? >> $O/c4_sharded.err
+timeout 900 python tests/c4_sharded_check.py > $O/c4_sharded.json 2> $O/c4_sharded.err; echo rc=$? >> $O/c4_sharded.err
