@@ -130,3 +130,32 @@ def test_python_binding_mirrors_abi_names():
         "prng_version")]
     missing = [s for s in compute if not callable(getattr(P, s, None))]
     assert not missing, missing
+
+
+def _build_c_check(tmp_path):
+    """tests/c_abi_check.c: include/ciprng.h as plain C99 (-pedantic), linked
+    against libciprng.so (and the oracle for the GPU comparison)."""
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import oracle
+
+    oracle.build()
+    libdir, odir = os.path.join(root, "paper_1112_5239_b200"), os.path.join(root, "oracle")
+    exe = str(tmp_path / "c_abi_check")
+    cmd = ["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(root, "include"),
+           os.path.join(root, "tests", "c_abi_check.c"), "-L", libdir, "-lciprng", "-L", odir, "-loracle",
+           f"-Wl,-rpath,{libdir}", f"-Wl,-rpath,{odir}", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_abi_from_plain_c(tmp_path):
+    """The boundary from plain C (no Python, no CUDA API, no GPU): the header
+    compiles as C99, the library links, host self-tests and argument errors
+    behave as include/ciprng.h states."""
+    exe = _build_c_check(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "C ABI OK host" in r.stdout
