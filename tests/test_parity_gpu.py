@@ -254,6 +254,27 @@ def test_v0_single_stream_jump(ns, seed, paper_defaults):
     assert info.store_path == (3 if ns[-1] >= 4096 else 1)
 
 
+def test_v0_jump_chunk_edges_and_resume():
+    """Chunk edges of the jump path (one chunk = 128 segments x 148 CTAs x
+    64 rounds on a 148-SM B200): exactly one chunk, one chunk + 1 round (a
+    second launch of a single round), and a resumed stream (set_state from
+    a checkpoint taken mid-way) continuing word for word."""
+    chunk = 128 * torch.cuda.get_device_properties(0).multi_processor_count * 64
+    info = _check(W.V0, W.SEEDS[0], 1, [chunk, chunk + 1, 4096])
+    assert info.store_path == 3
+    g = P.ChaoticPRNG(W.SEEDS[2], 1, W.V0)
+    g.generate(5000)
+    ck = g.get_state()
+    tail = P.as_u32(g.generate(9000))
+    g2 = P.ChaoticPRNG(W.SEEDS[0], 1, W.V0)
+    g2.set_state(ck)
+    assert np.array_equal(P.as_u32(g2.generate(9000)), tail)
+    st = O.states_from_planes(W.V0, ck)
+    assert np.array_equal(tail, O.generate(W.V0, st, 9000))
+    g.close()
+    g2.close()
+
+
 def test_v0_jump_equals_sequential_kernel(monkeypatch):
     """The jump path and the one-thread chain (CIPRNG_V0_JUMP=0) agree word
     for word at a size the oracle would take seconds on (8 * 10^6)."""
