@@ -226,14 +226,17 @@ CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_de
 CIPRNG_API int prng_battery(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
 
 /* Verification digest of one call's output block (reading Q28; a check
- * value defined by this build, the paper has none):
- * digest_dev[0] += sum over s < n_local, i < n of h(idx, out_dev[s*n + i])
- *   (mod 2^64), idx = (first_stream + s) * n + i,
- *   h(idx, x) = m(idx * 0x9E3779B97F4A7C15 + x),
- *   m(z) = z ^= z >> 32; z *= 0xD6E8FEB86659FD93; z ^= z >> 32.
- * Position-aware, additive across shards, and a bijection of each word for a
- * fixed position (one wrong word always changes the digest).  out_dev needs
- * only 4-byte alignment.  Errors: PRNG_EINVAL (NULL), PRNG_ECUDA. */
+ * value defined by this build, the paper has none).  Each stream's row is
+ * taken in word pairs (out[s*n + 2j], out[s*n + 2j + 1]), the lone last word
+ * of an odd row paired with 0, and
+ *   digest_dev[0] += sum over pairs of mix64((hi << 32 | lo) + P * G)
+ *   (mod 2^64), P = (first_stream + s) * ceil(n / 2) + j,
+ * mix64 = the SplitMix64 finaliser, G = 0x9E3779B97F4A7C15 -- output number
+ * P of SplitMix64 seeded with the pair.  Position-aware, additive across
+ * shards (rows are whole units), and a bijection of each pair for a fixed
+ * position (one wrong word always changes the digest).  out_dev needs 4-byte
+ * alignment (8-byte and an even n take the vectorised kernel).
+ * Errors: PRNG_EINVAL (NULL), PRNG_ECUDA. */
 CIPRNG_API int prng_digest(const uint32_t *out_dev, uint64_t first_stream, uint64_t n_local, uint64_t n,
                 uint64_t *digest_dev, void *stream);
 

@@ -35,8 +35,10 @@
  *                         published xor64 / pinned Listing-1 fold, I3 group
  *                         parity, single-cell injection, hand-traced C=2
  *   orc_stats_words       brute-force recount on tiny inputs; pi estimate
- *   orc_digest_words      parity unpinned (a verification hash defined by
- *                         this build; only its arithmetic is checked)
+ *   orc_digest_words      a verification hash defined by this build (Q28):
+ *                         single pairs pinned to the published SplitMix64
+ *                         sequence (h = output P of SplitMix64 seeded with
+ *                         the pair); shard additivity, injectivity
  *   orc_v*_init_words     word -> state mapping checked field by field
  *   (seeders)             against the published SplitMix64 generator (Q11);
  *                         zero guards reached by injected words and tied to
@@ -1024,25 +1026,21 @@ int orc_gamma_reach(const uint32_t *f, uint32_t n, uint64_t *report)
     return ORC_OK;
 }
 
-/* Verification digest (reading Q28, r2 definition): sum over the call's
- * words of h(idx, x_idx) mod 2^64, idx = (first_stream + s) * n + i,
- * h(idx, x) = m(idx * 0x9E3779B97F4A7C15 + x),
- * m(z) = z ^= z >> 32; z *= 0xD6E8FEB86659FD93; z ^= z >> 32. */
-static uint64_t orc_digest_mix(uint64_t z)
-{
-    z ^= z >> 32;
-    z *= 0xD6E8FEB86659FD93ull;
-    z ^= z >> 32;
-    return z;
-}
-
+/* Verification digest (reading Q28, r2 definition): each stream's row is
+ * taken in pairs (x_2j, x_2j+1), the lone last word of an odd row paired
+ * with 0, and the digest is the sum mod 2^64 over pairs of
+ * orc_mix64((x_2j+1 << 32 | x_2j) + P * 0x9E3779B97F4A7C15), with
+ * P = (first_stream + s) * ceil(n / 2) + j -- output number P of SplitMix64
+ * seeded with the pair (the finaliser and increment of orc_splitmix_word). */
 uint64_t orc_digest_words(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n)
 {
-    uint64_t s, i, acc = 0;
+    uint64_t s, j, acc = 0, hn = (n + 1) / 2;
     for (s = 0; s < n_local; s++)
-        for (i = 0; i < n; i++) {
-            uint64_t idx = (first_stream + s) * n + i;
-            acc += orc_digest_mix(idx * 0x9E3779B97F4A7C15ull + (uint64_t)out[s * n + i]);
+        for (j = 0; j < hn; j++) {
+            uint64_t lo = out[s * n + 2 * j];
+            uint64_t hi = (2 * j + 1 < n) ? out[s * n + 2 * j + 1] : 0;
+            uint64_t P = (first_stream + s) * hn + j;
+            acc += orc_mix64(((hi << 32) | lo) + P * 0x9E3779B97F4A7C15ull);
         }
     return acc;
 }

@@ -108,20 +108,22 @@ int launch_init(const InitArgs &a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ digest
-// Q28 (r2): d = sum_idx h(idx, x_idx) mod 2^64 with idx = global s*n + i and
-// h(idx, x) = m(idx * G + x), m(z) = { z ^= z >> 32; z *= K; z ^= z >> 32 }.
-// h is a bijection of x for a fixed idx (add, xorshift, odd multiply are all
-// invertible), so any single wrong word changes the digest.  Per word: one
-// 64-bit multiply (3 IMAD) and about 8 ALU ops -- about 9 TB/s of ALU
-// throughput on 148 SMs, above HBM, so the kernel streams at memory speed
-// (the r1 definition, two SplitMix64 finalisers per word, ran at 1.36 TB/s).
-// idx * G advances by G per word, so it is an add, not a multiply.
-constexpr uint64_t kDigestG = 0x9E3779B97F4A7C15ull, kDigestK = 0xD6E8FEB86659FD93ull;
+// Q28 (r2): the words of each stream's row are taken in pairs (x_2j, x_2j+1)
+// -- a lone last word of an odd row is paired with 0 -- and
+//   d = sum over pairs of mix64((x_2j+1 << 32 | x_2j) + P * G)  (mod 2^64),
+// P = global stream * ceil(n / 2) + j the pair's global position, mix64 the
+// SplitMix64 finaliser and G its increment: h is output number P of
+// SplitMix64 seeded with the pair, so the mixer is pinned by the published
+// SplitMix64 sequence.  For a fixed position h is a bijection of the pair
+// (add and mix64 are invertible), so any wrong word changes the digest; rows
+// are whole units, so shard digests add.  One finaliser per TWO words: ~9
+// ALU ops per word, above HBM speed on 148 SMs (one finaliser per word ran
+// at 3.6 TB/s, ALU bound; the r1 definition, two finalisers per word and
+// scalar loads, at 1.36 TB/s).  P * G advances by G per pair: an add.
+constexpr uint64_t kDigestG = 0x9E3779B97F4A7C15ull;
 
-__device__ __forceinline__ uint64_t digest_mix(uint64_t z) {
-    z ^= z >> 32;
-    z *= kDigestK;
-    return z ^ (z >> 32);
+__device__ __forceinline__ uint64_t digest_pair(uint32_t lo, uint32_t hi, uint64_t pg) {
+    return splitmix_fin(((uint64_t)hi << 32 | lo) + pg);
 }
 
 __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *p) {
@@ -132,50 +134,67 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint32_t *p) {
     return v;
 }
 
-// Thread t of the grid takes 16-byte chunks t, t + stride, ... (two in
-// flight per iteration); `head` scalar words before the first aligned chunk
-// and the ragged tail go to the first threads.
+__device__ __forceinline__ void digest_reduce(uint64_t acc, uint64_t *digest) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
+    if ((threadIdx.x & 31u) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long *>(digest), (unsigned long long)acc);
+}
+
+// Fast path: n even and out 8-byte aligned, so the block is a flat array of
+// pairs, pair k at global position first_stream * n/2 + k.  Thread t takes
+// 16-byte chunks (two pairs) t, t + stride, ... (two chunks in flight); a
+// head pair before the first 16-byte boundary and a tail pair go to thread 0.
 __global__ void __launch_bounds__(256) digest_kernel(const uint32_t *__restrict__ out, uint64_t first_stream,
                                                      uint64_t total, uint64_t n, uint64_t *digest) {
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t base = first_stream * n;  // global index of out[0]
-    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(out) >> 2) & 3u);
-    const uint64_t head = total < (uint64_t)((4u - mis) & 3u) ? total : (uint64_t)((4u - mis) & 3u);
-    const uint64_t chunks = (total - head) >> 2;
-    const uint32_t *body = out + head;
+    const uint64_t pairs = total >> 1;
+    const uint64_t p0 = first_stream * (n >> 1);  // global position of pair 0
+    const uint64_t head = (reinterpret_cast<uintptr_t>(out) & 8u) && pairs ? 1 : 0;
+    const uint64_t chunks = (pairs - head) >> 1;
+    const uint32_t *body = out + 2 * head;
     uint64_t acc = 0;
     uint64_t c = tid;
     for (; c + stride < chunks; c += 2 * stride) {
         const uint4 v0 = ld_stream_v4(body + 4 * c);
         const uint4 v1 = ld_stream_v4(body + 4 * (c + stride));
-        uint64_t g0 = (base + head + 4 * c) * kDigestG, g1 = (base + head + 4 * (c + stride)) * kDigestG;
-        acc += digest_mix(g0 + v0.x); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.y); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.z); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.w);
-        acc += digest_mix(g1 + v1.x); g1 += kDigestG;
-        acc += digest_mix(g1 + v1.y); g1 += kDigestG;
-        acc += digest_mix(g1 + v1.z); g1 += kDigestG;
-        acc += digest_mix(g1 + v1.w);
+        const uint64_t g0 = (p0 + head + 2 * c) * kDigestG, g1 = (p0 + head + 2 * (c + stride)) * kDigestG;
+        acc += digest_pair(v0.x, v0.y, g0);
+        acc += digest_pair(v0.z, v0.w, g0 + kDigestG);
+        acc += digest_pair(v1.x, v1.y, g1);
+        acc += digest_pair(v1.z, v1.w, g1 + kDigestG);
     }
     if (c < chunks) {
         const uint4 v0 = ld_stream_v4(body + 4 * c);
-        uint64_t g0 = (base + head + 4 * c) * kDigestG;
-        acc += digest_mix(g0 + v0.x); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.y); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.z); g0 += kDigestG;
-        acc += digest_mix(g0 + v0.w);
+        const uint64_t g0 = (p0 + head + 2 * c) * kDigestG;
+        acc += digest_pair(v0.x, v0.y, g0);
+        acc += digest_pair(v0.z, v0.w, g0 + kDigestG);
     }
-    // head words [0, head) and tail words [head + 4 chunks, total): at most 6
-    const uint64_t tail0 = head + 4 * chunks;
-    if (tid < head) acc += digest_mix((base + tid) * kDigestG + out[tid]);
-    if (tid < total - tail0) acc += digest_mix((base + tail0 + tid) * kDigestG + out[tail0 + tid]);
-#pragma unroll
-    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
-    if ((threadIdx.x & 31u) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long *>(digest), (unsigned long long)acc);
+    if (tid == 0) {
+        if (head) acc += digest_pair(out[0], out[1], p0 * kDigestG);
+        const uint64_t tl = head + 2 * chunks;  // at most one pair left
+        if (tl < pairs) acc += digest_pair(out[2 * tl], out[2 * tl + 1], (p0 + tl) * kDigestG);
+    }
+    digest_reduce(acc, digest);
+}
+
+// General path (n odd, or out not 8-byte aligned): pair k = (row, j) by
+// division, scalar loads; the lone last word of an odd row pairs with 0.
+__global__ void __launch_bounds__(256) digest_general_kernel(const uint32_t *__restrict__ out, uint64_t first_stream,
+                                                             uint64_t n_local, uint64_t n, uint64_t *digest) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const uint64_t hn = (n + 1) >> 1, pairs = n_local * hn;
+    uint64_t acc = 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pairs; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = k / hn, j = k - r * hn;
+        const uint32_t *row = out + r * n;
+        const uint32_t lo = row[2 * j], hi = 2 * j + 1 < n ? row[2 * j + 1] : 0u;
+        acc += digest_pair(lo, hi, ((first_stream + r) * hn + j) * kDigestG);
+    }
+    digest_reduce(acc, digest);
 }
 
 int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, uint64_t n, uint64_t *digest,
@@ -185,7 +204,10 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
     uint64_t blocks = (total / 8 + 255) / 256;  // two 16-byte chunks per thread per iteration
     if (blocks < 1) blocks = 1;
     if (blocks > (uint64_t)grid) blocks = grid;
-    launch_k(digest_kernel, dim3((int)blocks), dim3(256), 0, st, out, first_stream, total, n, digest);
+    if (n % 2 == 0 && reinterpret_cast<uintptr_t>(out) % 8 == 0)
+        launch_k(digest_kernel, dim3((int)blocks), dim3(256), 0, st, out, first_stream, total, n, digest);
+    else
+        launch_k(digest_general_kernel, dim3((int)blocks), dim3(256), 0, st, out, first_stream, n_local, n, digest);
     return 1;
 }
 

@@ -379,6 +379,21 @@ def test_digest_shard_additive():
     assert swapped[5, 2] != swapped[5, 3] and O.digest(swapped) != O.digest(out)
 
 
+def test_digest_pairs_are_published_splitmix64(golden):
+    """Q28: h = output number P of SplitMix64 seeded with the word pair (hi:lo),
+    P the pair's global position, so a one-pair row (seed, 0) -- or a lone
+    word of an odd row, paired with 0 -- at pair position k + 1 digests to the
+    k-th published SplitMix64 output for that seed (tests/golden: 1234567)."""
+    e = golden["published_sequences"]["splitmix64"]
+    assert e["seed"] < 2**32  # the seed fits the low word
+    for k, want in enumerate(e["outputs"]):
+        assert O.digest(np.array([[e["seed"], 0]], np.uint32), k + 1) == want  # n = 2: P = first_stream
+        assert O.digest(np.array([[e["seed"]]], np.uint32), k + 1) == want     # n = 1: lone word, hi = 0
+    # rows are whole units: rows 1..5 of a one-word-per-row block sum the sequence
+    rows = np.full((5, 1), e["seed"], np.uint32)
+    assert O.digest(rows, 1) == sum(e["outputs"]) % 2**64
+
+
 def test_digest_injective_in_word():
     """Q28: for a fixed position h(idx, .) is a bijection of the word (add,
     xorshift and odd multiply are invertible), so one wrong word always
