@@ -14,7 +14,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1112_5239_b200", "libciprng.so")
-KEYS = ["UTMASTG", "UBLKCP", "STS.128", "STG.E.128", "STG.E", "LDG", "SHFL.IDX", "ATOMS", "RED", "LOP3", "SHF",
+KEYS = ["UTMASTG", "UBLKCP", "STS.128", "STG.E.128", "STG.E", "LDG", "LDS", "SHFL.IDX", "ATOMS", "RED", "LOP3", "SHF",
         "IMAD.HI", "IMAD.WIDE", "IMAD.SHL", "IMAD", "VIADDMNMX", "VIMNMX", "FFMA", "DFMA", "BMSK"]
 # kernels behind the bench rows (demangled-name prefixes, store/consume instantiations)
 SHOW = ["v1_fast_kernel<ciprng::StoreSink, 32, 2, false>", "v1_band_kernel<2, 2>",
@@ -22,7 +22,7 @@ SHOW = ["v1_fast_kernel<ciprng::StoreSink, 32, 2, false>", "v1_band_kernel<2, 2>
         "comb_fast_kernel<ciprng::SrcXor64T<0>, ciprng::StatsSink", "v0_kernel<ciprng::StoreSink, false, 0>",
         "v0_kernel<ciprng::StoreSink, true, 0>", "v2_kernel<ciprng::StoreSink, 0u, true>",
         "v2_kernel<ciprng::StoreSink, 256u, true>", "v2_kernel<ciprng::StatsSink", "cbg_encrypt_kernel",
-        "alg1_kernel"]
+        "alg1_kernel", "v0_jump_kernel", "digest_kernel", "format_kernel"]
 
 
 def main():
