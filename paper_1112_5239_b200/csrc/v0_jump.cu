@@ -224,7 +224,8 @@ int v0_jump_selftest(uint64_t *mismatches, uint32_t *degrees) {
 // ------------------------------------------------------------------ kernel
 // Shared-memory windows: generator g's output sequence, window i = state
 // after i steps = words [i, i + kGenWords[g]).  Each array ends in zero
-// words: the padding entries of the jump lists point there.
+// words: the sweep's sliding window reads up to 64 * ceil(deg / 64) + W - 1
+// (the polynomial bits past deg are zero, so those words never count).
 constexpr uint32_t kZ1 = kJumpMaxDeg[0], kZ2 = kJumpMaxDeg[1] + 3, kZ3 = kJumpMaxDeg[2] + 4;
 struct JumpSmem {
     uint64_t w1[kZ1 + 1];
