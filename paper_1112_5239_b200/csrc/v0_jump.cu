@@ -233,6 +233,8 @@ struct JumpSmem {
     uint64_t w3[kZ3 + 5];
     uint64_t part[kJumpThreads / 32][10];
     uint64_t bstart[10];
+    uint64_t bpoly[3][kJumpPolyWords];  // this block's level-1 polynomials
+    uint32_t st0[24];                   // the chunk-start state planes
     uint32_t warp_tot[kJumpThreads / 32];
     uint32_t block_base;
 };
@@ -315,35 +317,54 @@ __device__ __forceinline__ void krylov_windows(JumpSmem &sm, const uint64_t (&s1
     }
 }
 
-// acc ^= sum over the set bits i of this thread's jump polynomial of window
-// i of w (W words).  Every lane of a warp walks the SAME window index i at
-// the same time -- a broadcast shared load, one wavefront -- and keeps the W
-// words of the window in registers, sliding it by one word per index; the
-// lane's own bit masks the XOR.  (Gathering only the set bits' windows made
-// every load a 32-address gather: ~7 bank-conflicted wavefronts per load,
-// 4x slower.)  The polynomial words of the T thread slots are interleaved
-// ([q][t]) so the warp's poly load is coalesced.
+// Level-2 jump by the "method of four Russians": the windows are taken in
+// chunks of four (indices 4c .. 4c+3) and for every chunk the 16 XOR
+// combinations of its four windows are tabulated in shared memory,
+// tab[c][k][p] = XOR over the set bits j of p of word k of window 4c + j.
+// A thread then applies its polynomial one NIBBLE at a time: one table load
+// and one XOR per state word per four bits, against 4 masked XORs per word
+// in a bit-by-bit sweep (which was ALU bound: 11.8 of 27 us per C1 call).
+// The 16 entries of tab[c][k] are 128 contiguous bytes -- one per bank pair
+// -- so lanes reading different nibbles never conflict and equal nibbles
+// broadcast.
+constexpr uint32_t kTab1 = kJumpMaxDeg[0] / 4, kTab2 = kJumpMaxDeg[1] / 4, kTab3 = kJumpMaxDeg[2] / 4;
+constexpr size_t kTabWords = (size_t)16 * (kTab1 * 1 + kTab2 * 4 + kTab3 * 5);
+
+// Build generator g's tables: thread t computes entries (2t, 2t + 1),
+// (2t + 2T, 2t + 2T + 1), ... of the flat [chunk][word][16] array -- each an
+// XOR of at most four window words (broadcast loads: neighbouring threads
+// share the chunk) -- so a warp's stores cover 256 contiguous bytes.
+template <int W>
+__device__ __forceinline__ void build_tables(const uint64_t *w, uint32_t chunks, uint64_t *tab) {
+    const uint32_t pairs = chunks * W * 8;  // two entries per pair
+    for (uint32_t e2 = threadIdx.x; e2 < pairs; e2 += blockDim.x) {
+        const uint32_t ck = e2 >> 3, p0 = (e2 & 7u) * 2;  // (chunk, word) and the even pattern
+        const uint32_t c = ck / W, k = ck - c * W;
+        const uint64_t *wc = w + 4 * c + k;
+        uint64_t even = 0;
+        if (p0 & 2) even ^= wc[1];
+        if (p0 & 4) even ^= wc[2];
+        if (p0 & 8) even ^= wc[3];
+        const uint64_t odd = even ^ wc[0];  // p0 + 1 adds window 4c
+        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(tab + 2 * (size_t)e2)), "l"(even), "l"(odd)
+                     : "memory");
+    }
+}
+
 template <int W, int Q>
-__device__ __forceinline__ void jump_sweep(const uint64_t *w, const uint64_t (&poly)[Q], uint32_t deg, uint64_t *acc) {
-    uint64_t win[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) win[k] = w[k];
+__device__ __forceinline__ void jump_tab(const uint64_t *tab, const uint64_t (&poly)[Q], uint32_t deg, uint64_t *acc) {
 #pragma unroll 1
     for (uint32_t q = 0; q < (uint32_t)Q && q * 64 < deg; ++q) {
         uint64_t bits = 0;
 #pragma unroll
         for (int r = 0; r < Q; ++r)
             if (r == (int)q) bits = poly[r];
-        const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+        const uint64_t *tq = tab + (size_t)q * 16 * W * 16;  // 16 chunks per poly word
 #pragma unroll
-        for (uint32_t j = 0; j < 64; ++j) {
-            const uint32_t half = j < 32 ? lo : hi;
-            const uint64_t m = (uint64_t)(int64_t)((int32_t)(half << (31 - (j & 31))) >> 31);
+        for (uint32_t j = 0; j < 16; ++j) {
+            const uint32_t nib = (uint32_t)(bits >> (4 * j)) & 15u;
 #pragma unroll
-            for (int k = 0; k < W; ++k) acc[k] ^= win[k] & m;
-#pragma unroll
-            for (int k = 0; k + 1 < W; ++k) win[k] = win[k + 1];
-            win[W - 1] = w[q * 64 + j + W];
+            for (int k = 0; k < W; ++k) acc[k] ^= tq[(j * W + k) * 16 + nib];
         }
     }
 }
@@ -363,12 +384,25 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
 #pragma unroll
     for (int q = 0; q < 5; ++q) pj3[q] = __ldg(a.poly + 2 * PW + (size_t)q * T + t);
 
+    // this block's level-1 polynomials (z^(b T L)) into shared memory now, so
+    // the level-1 pass after the first Krylov phase reads no global memory
+    if (t < 3 * kJumpPolyWords) {
+        const uint32_t g = t / kJumpPolyWords, q = t % kJumpPolyWords;
+        sm.bpoly[g][q] = __ldg(a.poly + g * PW + (size_t)T * kJumpPolyWords + (size_t)b * kJumpPolyWords + q);
+    }
+
     // chunk start state (words: a, b0..b3, c0..c4), d, x
+    // One coalesced load per CTA (lanes 0..22 of warp 0), shared through
+    // shared memory: every thread loading the 23 words itself sent 13 k
+    // requests for one cache line from all CTAs to one L2 slice -- ~4 us of
+    // queueing at the start of every call (found with -DCIPRNG_JUMP_TIMING).
+    if (t < 23) sm.st0[t] = a.state[t];
+    __syncthreads();
     uint64_t s0[10];
 #pragma unroll
-    for (int k = 0; k < 10; ++k) s0[k] = (uint64_t)a.state[2 * k] | ((uint64_t)a.state[2 * k + 1] << 32);
-    const uint64_t d0 = (uint64_t)a.state[20] | ((uint64_t)a.state[21] << 32);
-    const uint32_t x0 = a.state[22];
+    for (int k = 0; k < 10; ++k) s0[k] = (uint64_t)sm.st0[2 * k] | ((uint64_t)sm.st0[2 * k + 1] << 32);
+    const uint64_t d0 = (uint64_t)sm.st0[20] | ((uint64_t)sm.st0[21] << 32);
+    const uint32_t x0 = sm.st0[22];
 
     // level 1: this block's start = z^(b T L) applied to the chunk start.
     // Every thread takes a slice of the list; XOR-reduce over the block.
@@ -380,28 +414,38 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
         uint64_t part[10];
 #pragma unroll
         for (int k = 0; k < 10; ++k) part[k] = 0;
-        const size_t boff = (size_t)T * kJumpPolyWords + (size_t)b * kJumpPolyWords;  // block slot b
-        const uint64_t *q1 = a.poly + boff, *q2 = a.poly + PW + boff, *q3 = a.poly + 2 * PW + boff;
-        for (uint32_t i = t; i < a.deg[0]; i += T)
+        // <= 3 iterations per generator: NOT unrolled.  This code runs once
+        // per warp, so its size is its cost -- ptxas' 8-way unrolled copy
+        // (21 KB of SASS) took 5.1 us of instruction-cache misses per call
+        const uint64_t *q1 = sm.bpoly[0], *q2 = sm.bpoly[1], *q3 = sm.bpoly[2];
+#pragma unroll 1
+        for (uint32_t i = t; i < kZ1; i += T)  // bits past deg are 0
             if ((q1[i >> 6] >> (i & 63)) & 1u) part[0] ^= sm.w1[i];
-        for (uint32_t i = t; i < a.deg[1]; i += T)
+        JT(12);
+#pragma unroll 1
+        for (uint32_t i = t; i < kZ2 - 3; i += T)
             if ((q2[i >> 6] >> (i & 63)) & 1u)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) part[1 + k] ^= sm.w2[i + k];
-        for (uint32_t i = t; i < a.deg[2]; i += T)
+        JT(13);
+#pragma unroll 1
+        for (uint32_t i = t; i < kZ3 - 4; i += T)
             if ((q3[i >> 6] >> (i & 63)) & 1u)
 #pragma unroll
                 for (int k = 0; k < 5; ++k) part[5 + k] ^= sm.w3[i + k];
+        JT(9);
 #pragma unroll
         for (int k = 0; k < 10; ++k) {
 #pragma unroll
             for (int dlt = 16; dlt; dlt >>= 1) part[k] ^= __shfl_xor_sync(kFull, part[k], dlt);
         }
+        JT(10);
         if (lane == 0)
 #pragma unroll
             for (int k = 0; k < 10; ++k) sm.part[warp][k] = part[k];
     }
     __syncthreads();
+    JT(11);
     if (t < 10) {
         uint64_t v = 0;
         for (uint32_t w = 0; w < T / 32; ++w) v ^= sm.part[w][t];
@@ -417,12 +461,18 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     krylov_windows(sm, sb, a);
     __syncthreads();
     JT(3);
+    uint64_t *tab1 = reinterpret_cast<uint64_t *>(stage + (size_t)T * L);  // after the staging area
+    uint64_t *tab2 = tab1 + (size_t)16 * kTab1, *tab3 = tab2 + (size_t)16 * kTab2 * 4;
+    build_tables<1>(sm.w1, (a.deg[0] + 3) / 4, tab1);
+    build_tables<4>(sm.w2, (a.deg[1] + 3) / 4, tab2);
+    build_tables<5>(sm.w3, (a.deg[2] + 3) / 4, tab3);
+    __syncthreads();
     uint64_t s[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) s[k] = 0;
-    jump_sweep<1>(sm.w1, pj1, a.deg[0], s);
-    jump_sweep<4>(sm.w2, pj2, a.deg[1], s + 1);
-    jump_sweep<5>(sm.w3, pj3, a.deg[2], s + 5);
+    jump_tab<1>(tab1, pj1, a.deg[0], s);
+    jump_tab<4>(tab2, pj2, a.deg[1], s + 1);
+    jump_tab<5>(tab3, pj3, a.deg[2], s + 5);
 
     JT(4);
     // generate this segment as a local prefix XOR
@@ -519,7 +569,9 @@ void v0_jump_free(V0JumpPlan &p) {
 }
 
 static size_t jump_smem(uint32_t L) {
-    return ((sizeof(JumpSmem) + 15) & ~size_t(15)) + (size_t)kJumpThreads * L * 4;
+    // staging area (T * L words, padded to 16 bytes), then the nibble tables
+    return ((sizeof(JumpSmem) + 15) & ~size_t(15)) + (((size_t)kJumpThreads * L * 4 + 15) & ~size_t(15)) +
+           kTabWords * 8;
 }
 
 // (Re)build the plan for (L, B): polynomials z^(t L), t < T (thread slots,
@@ -645,6 +697,14 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
             fprintf(stderr, "jump phases (us, latest CTA, from the first start): start %.2f krylov1 %.2f lvl1 %.2f "
                     "krylov2 %.2f sweep %.2f gen %.2f scan %.2f lookback %.2f write %.2f\n",
                     mx[0], mx[1], mx[2], mx[3], mx[4], mx[5], mx[6], mx[7], mx[8]);
+            // per-CTA phase durations: median and max over CTAs
+            for (int k : {1, 12, 13, 9, 10, 11, 2, 3, 4, 5, 6, 7, 8}) {
+                std::vector<double> dd;
+                const int kp = k == 12 ? 1 : k == 13 ? 12 : k == 9 ? 13 : k == 10 ? 9 : k == 11 ? 10 : k == 2 ? 11 : k - 1;
+                for (uint32_t bb = 0; bb < blocks; ++bb) dd.push_back((double)(h[bb * 16 + k] - h[bb * 16 + kp]) * 1e-3);
+                std::sort(dd.begin(), dd.end());
+                fprintf(stderr, "  phase %d: median %.2f max %.2f us\n", k, dd[dd.size() / 2], dd.back());
+            }
         }
 #endif
     }
