@@ -255,11 +255,13 @@ struct JumpArgs {
 
 // Phase timestamps (diagnostic builds, -DCIPRNG_JUMP_TIMING): thread 0 of
 // every CTA records %globaltimer at each phase boundary; the host prints the
-// latest CTA's time per phase.  Measured (r2, 10^6 numbers, 27 us): Krylov
-// windows 1.9, block jump 4.5, Krylov again 1.6, thread sweeps 11.8,
-// generation 2.7, scans + look-back 3.6, write 0.5 us -- the sweeps are ALU
-// bound (math-throttle stalls; splitting each segment's sweep over 4 threads
-// did not help, 30.7 us per call).
+// latest CTA's time per phase (the timestamp stores themselves can queue
+// behind pending loads, so a phase right after a barrier may absorb their
+// latency).  Measured (r2, 10^6 numbers, 24.8 us per call): Krylov windows
+// 1.7, block jump 3.0, Krylov again 1.7, table build 4.7, nibble lookups 3.2,
+// generation 2.6, scans + look-back 2.5, write 0.5 us.  Tried and slower: a
+// bit-by-bit sweep (11.8 us, ALU bound), the sweep split over 4 threads per
+// segment (30.7 us per call), a branch-free masked table build (26.6 us).
 #if defined(CIPRNG_JUMP_TIMING)
 #define JT(k)                                                              \
     do {                                                                   \
