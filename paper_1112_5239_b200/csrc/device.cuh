@@ -46,7 +46,19 @@ __device__ __forceinline__ uint32_t shr_fma(uint32_t v) {
 // 13 / 2; both right shifts as IMAD.HI: 9 / 10).
 __device__ __forceinline__ uint32_t xor128_f(uint32_t xk, uint32_t wk3) {
     uint32_t t = xk ^ (xk << 11);
+#if defined(CIPRNG_EXP_X128_ALL_HI)  // experiment: both right shifts as IMAD.HI (heavy FMA)
+    return (wk3 ^ shr_fma<19>(wk3)) ^ (t ^ shr_fma<8>(t));
+#else
     return (wk3 ^ shr_fma<19>(wk3)) ^ (t ^ (t >> 8));
+#endif
+}
+// The same with both right shifts on SHF (ALU): the V1 fused consumer, whose
+// pi-pair test is IMAD.WIDE-heavy, balances its pipes better this way --
+// 1.816 -> 1.847e12 numbers/s; both shifts as IMAD.HI 1.740e12
+// (profiles/experiments/s53_x128_shifts.jsonl).
+__device__ __forceinline__ uint32_t xor128_f_alu(uint32_t xk, uint32_t wk3) {
+    uint32_t t = xk ^ (xk << 11);
+    return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
 }
 // Same on 64-bit words (Listing 1's xor128, reading Q2).
 __host__ __device__ __forceinline__ uint64_t xor128_f64(uint64_t xk, uint64_t wk3) {

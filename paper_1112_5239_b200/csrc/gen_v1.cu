@@ -91,6 +91,14 @@ __global__ void __launch_bounds__(256) v1_general_kernel(GenArgs a) {
 // j = L & 15, owns rows rA = 32h + j and rB = rA + 16 of the tile.
 constexpr int kFastTileRows = 64;
 
+// xor128 step of the fast kernel: the fused consumer takes the all-ALU-shift
+// form (device.cuh xor128_f_alu), the store and battery kernels the balanced one
+template <class Sink>
+__device__ __forceinline__ uint32_t v1_x128(uint32_t xk, uint32_t wk3) {
+    if constexpr (std::is_same<Sink, StatsSink>::value) return xor128_f_alu(xk, wk3);
+    else return xor128_f(xk, wk3);
+}
+
 
 // kCols == 0: direct stores through the Sink (StoreSink: 128-bit STG per
 // 4 rounds per stream; StatsSink: fused consumer).  kCols in {8, 16, 32}:
@@ -192,8 +200,8 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
         uint32_t nb = 0;
 
 #define CIPRNG_V1_ROUND(GA, GA3, GB, GB3, OA, OB)        \
-    GA = xor128_f(GA, GA3);                              \
-    GB = xor128_f(GB, GB3);                              \
+    GA = v1_x128<Sink>(GA, GA3);                              \
+    GB = v1_x128<Sink>(GB, GB3);                              \
     nb = __shfl_sync(kFull, u, src, 16);                 \
     xA ^= GA ^ nb;                                       \
     xB ^= GB ^ nb;                                       \
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
             i = nb4;
             if constexpr (kStg) {
                 for (; i < a.n; ++i) {  // the last n % 4 rounds: scalar stores
-                    uint32_t gA = xor128_f(a0, a3), gB = xor128_f(b0, b3);
+                    uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128<Sink>(b0, b3);
                     a0 = a1; a1 = a2; a2 = a3; a3 = gA;
                     b0 = b1; b1 = b2; b2 = b3; b3 = gB;
                     nb = __shfl_sync(kFull, u, src, 16);
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
             }
 #undef CIPRNG_V1_DIRECT4
             for (; i < a.n; ++i) {  // ragged tail
-                uint32_t gA = xor128_f(a0, a3), gB = xor128_f(b0, b3);
+                uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128<Sink>(b0, b3);
                 a0 = a1; a1 = a2; a2 = a3; a3 = gA;
                 b0 = b1; b1 = b2; b2 = b3; b3 = gB;
                 nb = __shfl_sync(kFull, u, src, 16);
