@@ -57,7 +57,13 @@ __device__ __forceinline__ uint32_t xor128_f(uint32_t xk, uint32_t wk3) {
 // 1.816 -> 1.847e12 numbers/s; both shifts as IMAD.HI 1.740e12
 // (profiles/experiments/s53_x128_shifts.jsonl).
 __device__ __forceinline__ uint32_t xor128_f_alu(uint32_t xk, uint32_t wk3) {
+#if defined(CIPRNG_EXP_X128_SHL_ALU)  // experiment: the left shift on SHF too: 1.840 -> 1.698e12 (s54), off
+    uint32_t sh;
+    asm("shf.l.clamp.b32 %0, %1, %2, 11;" : "=r"(sh) : "r"(0u), "r"(xk));
+    uint32_t t = xk ^ sh;
+#else
     uint32_t t = xk ^ (xk << 11);
+#endif
     return (wk3 ^ (wk3 >> 19)) ^ (t ^ (t >> 8));
 }
 // Same on 64-bit words (Listing 1's xor128, reading Q2).

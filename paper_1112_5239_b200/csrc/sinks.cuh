@@ -175,6 +175,9 @@ struct StatsSink {
 #if defined(CIPRNG_EXP_BIN_HI)  // experiment: x >> 24 as IMAD.HI (FMA pipe) instead of SHF (ALU):
         // V1 -4 %, V3 -0.8 %, V0 +0.3 % (profiles/experiments/s40_consume_bin_hi.jsonl), off
         asm("{\n\t.reg .u32 b;\n\tmul.hi.u32 b, %1, 256;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
+#elif defined(CIPRNG_EXP_BIN_LEA)  // experiment: the scaled add as LEA (ALU) instead of IMAD (heavy FMA):
+        // V1 1.840 -> 1.667e12, V3 -6 % (profiles/experiments/s54_consumer_pipes.jsonl), off
+        addr = base + ((o >> 24) << 2);
 #else
         asm("{\n\t.reg .u32 b;\n\tshr.u32 b, %1, 24;\n\tmad.lo.u32 %0, b, 4, %2;\n\t}" : "=r"(addr) : "r"(o), "r"(base));
 #endif
