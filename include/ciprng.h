@@ -95,9 +95,9 @@ enum prng_store_path {
                               by cp.async.bulk.tensor (V1 default tables,
                               n % 4 == 0); falls back to DIRECT otherwise */
     PRNG_STORE_JUMP = 3    /* reported by prng_get_info only: a V0 handle
-                              with ONE stream and n >= 4096 splits the
-                              stream over the GPU by GF(2) jump-ahead of
-                              its generators + an XOR scan of x (same
+                              with at most 16 streams and n >= 4096 splits
+                              each stream over the GPU by GF(2) jump-ahead
+                              of its generators + an XOR scan of x (same
                               words; BASELINE configs[0] / C1) */
 };
 

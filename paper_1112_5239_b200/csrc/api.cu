@@ -264,8 +264,9 @@ int run_pass(prng_t *h, uint64_t n, uint64_t s_begin, uint64_t s_count, uint32_t
     int path = PRNG_STORE_DIRECT;
     if (h->variant == 0) {
         int jl = -1;
-        if (mode == 0 && h->jump_on && h->n_local == 1 && s_count == 1 && n >= kJumpMinN)
-            jl = v0_jump_launch(h->jump, h->state, out, n, st);
+        if (mode == 0 && h->jump_on && h->n_local <= kJumpMaxStreams && s_begin == 0 && s_count == h->n_local &&
+            n >= kJumpMinN)
+            jl = v0_jump_launch(h->jump, h->state, h->n_local, out, n, st);
         if (jl == -4) return cuda_fail(cudaErrorLaunchFailure);
         if (jl > 0) path = PRNG_STORE_JUMP;
         launches = jl > 0 ? jl : launch_v0(a, mode, st);

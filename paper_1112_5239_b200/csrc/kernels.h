@@ -156,10 +156,11 @@ constexpr int kJumpPolyWords = 6;
 constexpr int kJumpMaxDeg[3] = {64, 256, 320};  // state bits of xor64, xor128-64, xorwow-64
 constexpr uint32_t kJumpMaxL = 64;              // rounds per segment (shared-memory staging)
 constexpr uint64_t kJumpMinN = 4096;            // below this the one-thread chain is as fast
+constexpr uint64_t kJumpMaxStreams = 16;        // streams per handle the split path takes (grid rows)
 struct V0JumpPlan {
     uint64_t *poly = nullptr;   // jump polynomials (v0_jump.cu)
     uint32_t *flags = nullptr;  // [B] look-back flags, then [B] block aggregates
-    uint32_t L = 0, B = 0, epoch = 0;
+    uint32_t L = 0, B = 0, epoch = 0, streams = 0;
     uint64_t n = 0;    // rounds of the call the launch shape was chosen for
     size_t smem = 0;
 };
@@ -168,7 +169,7 @@ int v0_jump_selftest(uint64_t *mismatches, uint32_t *degrees);  // host only
 // >= 1: launches enqueued; -1..-3: not applicable / nothing enqueued (the
 // caller falls back to the one-thread kernel); -4: a later chunk failed to
 // launch after earlier chunks ran (the call fails, PRNG_ECUDA)
-int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st);
+int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint64_t n_local, uint32_t *out, uint64_t n, cudaStream_t st);
 void v0_jump_free(V0JumpPlan &p);
 
 // emit.cu: format 1 = hex lines (9 B per word), 2 = bit lines (33 B per word)

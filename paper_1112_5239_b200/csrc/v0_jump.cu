@@ -240,8 +240,10 @@ struct JumpSmem {
 };
 
 struct JumpArgs {
-    uint32_t *state;        // V0 SoA planes of ONE stream (23 words)
-    uint32_t *out;          // this chunk's first word
+    uint32_t *state;        // V0 SoA planes: word k of stream s at state[k * state_stride + s]
+    uint64_t state_stride;  // = n_local
+    uint32_t *out;          // this chunk's first word of stream 0; stream s at out + s * out_stride
+    uint64_t out_stride;    // = n (rounds per stream of the whole call)
     uint64_t n_chunk;       // rounds in this chunk
     const uint64_t *poly;   // jump polynomials, generator g at poly + g * (T + B) * kJumpPolyWords:
                             // thread slots [q][t], then block slots [b][q]
@@ -265,7 +267,7 @@ struct JumpArgs {
 #if defined(CIPRNG_JUMP_TIMING)
 #define JT(k)                                                              \
     do {                                                                   \
-        if (t == 0 && a.dbg) {                                             \
+        if (t == 0 && blockIdx.y == 0 && a.dbg) {                          \
             unsigned long long ts;                                         \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));         \
             a.dbg[b * 16 + (k)] = ts;                                      \
@@ -375,7 +377,12 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     extern __shared__ __align__(16) uint8_t jsm_raw[];
     JumpSmem &sm = *reinterpret_cast<JumpSmem *>(jsm_raw);
     uint32_t *stage = reinterpret_cast<uint32_t *>(jsm_raw + ((sizeof(JumpSmem) + 15) & ~size_t(15)));
+    // grid: x = CTA of the stream's segment range, y = stream (one stream per
+    // grid row; each row has its own look-back flags)
     const uint32_t T = kJumpThreads, t = threadIdx.x, b = blockIdx.x, L = a.L;
+    const uint64_t sid = blockIdx.y;
+    uint32_t *const flags = a.flags + sid * a.B, *const aggs = a.aggs + sid * a.B;
+    uint32_t *const out = a.out + sid * a.out_stride;
     const uint32_t lane = t & 31u, warp = t >> 5;
     const size_t PW = (size_t)(T + a.B) * kJumpPolyWords;  // poly words per generator
     // this thread's level-2 jump polynomials (z^(t L)), loaded early
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     // shared memory: every thread loading the 23 words itself sent 13 k
     // requests for one cache line from all CTAs to one L2 slice -- ~4 us of
     // queueing at the start of every call (found with -DCIPRNG_JUMP_TIMING).
-    if (t < 23) sm.st0[t] = a.state[t];
+    if (t < 23) sm.st0[t] = a.state[t * a.state_stride + sid];
     __syncthreads();
     uint64_t s0[10];
 #pragma unroll
@@ -518,16 +525,16 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     // publish this block's aggregate, then look back over the earlier blocks
     // (all co-resident: cooperative launch)
     if (t == 0) {
-        a.aggs[b] = agg;
+        aggs[b] = agg;
         __threadfence();
-        atomicExch(a.flags + b, a.epoch);
+        atomicExch(flags + b, a.epoch);
     }
     uint32_t prev = 0;
     for (uint32_t j = t; j < b; j += T) {
-        while (atomicAdd(a.flags + j, 0u) != a.epoch) {
+        while (atomicAdd(flags + j, 0u) != a.epoch) {
         }
         __threadfence();
-        prev ^= *reinterpret_cast<volatile uint32_t *>(a.aggs + j);
+        prev ^= *reinterpret_cast<volatile uint32_t *>(aggs + j);
     }
 #pragma unroll
     for (int dlt = 16; dlt; dlt >>= 1) prev ^= __shfl_xor_sync(kFull, prev, dlt);
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     const uint64_t blk0 = (uint64_t)b * T * L;
     const uint64_t blen =
         blk0 >= a.n_chunk ? 0 : (a.n_chunk - blk0 < (uint64_t)T * L ? a.n_chunk - blk0 : (uint64_t)T * L);
-    for (uint64_t k = t; k < blen; k += T) a.out[blk0 + k] = stage[k];
+    for (uint64_t k = t; k < blen; k += T) out[blk0 + k] = stage[k];
 
     JT(8);
     // state after the chunk: owned by the segment holding its last round
@@ -556,10 +563,10 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
         const uint64_t v[11] = {ra, rb0, rb1, rb2, rb3, rc0, rc1, rc2, rc3, rc4, rd};
 #pragma unroll
         for (int k = 0; k < 11; ++k) {
-            a.state[2 * k] = (uint32_t)v[k];
-            a.state[2 * k + 1] = (uint32_t)(v[k] >> 32);
+            a.state[(2 * k) * a.state_stride + sid] = (uint32_t)v[k];
+            a.state[(2 * k + 1) * a.state_stride + sid] = (uint32_t)(v[k] >> 32);
         }
-        a.state[22] = base ^ xl;
+        a.state[22 * a.state_stride + sid] = base ^ xl;
     }
 }
 
@@ -579,7 +586,7 @@ static size_t jump_smem(uint32_t L) {
 // (Re)build the plan for (L, B): polynomials z^(t L), t < T (thread slots,
 // interleaved [q][t]) and z^(b T L), b < B (block slots, [b][q]), as
 // kJumpPolyWords-word bit masks per generator.
-static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t B) {
+static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t B, uint32_t streams) {
     const uint32_t T = kJumpThreads;
     v0_jump_free(p);
     const size_t PW = (size_t)(T + B) * kJumpPolyWords;
@@ -602,27 +609,30 @@ static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t
         }
     }
     if (cudaMalloc(&p.poly, host.size() * 8) != cudaSuccess) return -2;
-    if (cudaMalloc(&p.flags, (size_t)2 * B * 4) != cudaSuccess) return -2;
+    if (cudaMalloc(&p.flags, (size_t)2 * streams * B * 4) != cudaSuccess) return -2;
     cudaMemcpy(p.poly, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
-    cudaMemset(p.flags, 0, (size_t)2 * B * 4);
+    cudaMemset(p.flags, 0, (size_t)2 * streams * B * 4);
     p.L = L;
     p.B = B;
+    p.streams = streams;
     p.epoch = 0;
     return 0;
 }
 
-int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cudaStream_t st) {
+int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint64_t n_local, uint32_t *out, uint64_t n, cudaStream_t st) {
     const MinPolys &mp = min_polys();
-    if (!mp.ok || n == 0) return -1;
+    if (!mp.ok || n == 0 || n_local == 0 || n_local > kJumpMaxStreams) return -1;
     const uint32_t T = kJumpThreads;
     // The device queries below cost more host time than the kernel runs, so
     // they are made once per plan; a call with the plan's n reuses it as is.
-    if (!(p.poly && p.n == n)) {
+    if (!(p.poly && p.n == n && p.streams == n_local)) {
         int dev = 0, sms = 148, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // CTAs per stream: the SMs shared among the streams (one grid row each)
+        const uint64_t per_stream = std::max<uint64_t>(1, (uint64_t)sms / n_local);
         // L: about one segment per thread of one CTA per SM, 16..kJumpMaxL rounds
-        uint64_t L = (n + (uint64_t)T * sms - 1) / ((uint64_t)T * sms);
+        uint64_t L = (n + (uint64_t)T * per_stream - 1) / ((uint64_t)T * per_stream);
         L = L < 16 ? 16 : (L > kJumpMaxL ? kJumpMaxL : L);
         const size_t smem = jump_smem((uint32_t)L);
         if (cudaFuncSetAttribute(v0_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -631,10 +641,11 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v0_jump_kernel, T, smem);
         if (per_sm < 1) return -1;
         uint64_t B = (n + T * L - 1) / (T * L);
-        const uint64_t maxB = (uint64_t)sms * (uint64_t)per_sm;
+        const uint64_t maxB = (uint64_t)sms * (uint64_t)per_sm / n_local;  // co-resident, all streams
+        if (maxB < 1) return -1;
         if (B > maxB) B = maxB;
-        if (!(p.poly && p.L == L && p.B == B)) {
-            const int rc = v0_jump_build(p, mp, (uint32_t)L, (uint32_t)B);
+        if (!(p.poly && p.L == L && p.B == B && p.streams == n_local)) {
+            const int rc = v0_jump_build(p, mp, (uint32_t)L, (uint32_t)B, (uint32_t)n_local);
             if (rc < 0) return rc;
         }
         p.n = n;
@@ -647,14 +658,16 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
     for (uint64_t r = 0; r < n; r += chunk) {
         JumpArgs ja;
         ja.state = state;
+        ja.state_stride = n_local;
         ja.out = out + r;
+        ja.out_stride = n;
         ja.n_chunk = n - r < chunk ? n - r : chunk;
         ja.poly = p.poly;
         for (int g = 0; g < 3; ++g) ja.deg[g] = (uint32_t)mp.deg[g];
         ja.L = p.L;
         ja.B = p.B;
         ja.flags = p.flags;
-        ja.aggs = p.flags + p.B;
+        ja.aggs = p.flags + n_local * p.B;
         ja.dbg = nullptr;
 #if defined(CIPRNG_JUMP_TIMING)
         static unsigned long long *dbg = nullptr;
@@ -667,7 +680,7 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint32_t *out, uint64_t n, cu
         // cooperative: the look-back spins on earlier blocks' flags
         const uint32_t blocks = (uint32_t)((ja.n_chunk + (uint64_t)T * L - 1) / ((uint64_t)T * L));
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(blocks);
+        cfg.gridDim = dim3(blocks, (uint32_t)n_local);
         cfg.blockDim = dim3(T);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;

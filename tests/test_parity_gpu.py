@@ -254,6 +254,21 @@ def test_v0_single_stream_jump(ns, seed, paper_defaults):
     assert info.store_path == (3 if ns[-1] >= 4096 else 1)
 
 
+@pytest.mark.parametrize("S,first", [(2, 0), (3, 7), (16, 0), (16, 1000)])
+def test_v0_few_streams_jump(S, first):
+    """A handle with up to 16 V0 streams takes the split path too (one grid
+    row of CTAs per stream, its own look-back): every stream equals the
+    oracle's sequential chain, over calls and with a shard offset."""
+    info = _check(W.V0, W.SEEDS[0], S, [5000, 70001], first=first)
+    assert info.store_path == 3
+
+
+def test_v0_seventeen_streams_use_the_stream_kernel():
+    """Past 16 streams the ordinary one-thread-per-stream kernel runs."""
+    info = _check(W.V0, W.SEEDS[1], 17, [5000])
+    assert info.store_path != 3
+
+
 def test_v0_jump_chunk_edges_and_resume():
     """Chunk edges of the jump path (one chunk = 128 segments x 148 CTAs x
     64 rounds on a 148-SM B200): exactly one chunk, one chunk + 1 round (a
