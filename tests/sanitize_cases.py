@@ -96,6 +96,7 @@ def case_jump():
     # block scans, cooperative look-back); 3 CTAs of 128 segments x 16 rounds
     for n in (5000, 4096):
         _gen(P.V0, n, S_=1)
+    _gen(P.V0, 5000, S_=3)  # three streams: three CTA rows, separate look-backs
     g = P.ChaoticPRNG(0, 1, P.V0, paper_defaults=True)
     st = O.init_states(P.V0, 0, 0, 1, paper_defaults=True)
     got = P.as_u32(g.generate(6000))
