@@ -127,6 +127,20 @@ int ciprng::resident_blocks(const void *kern, int threads, size_t smem) {
     return cache[key] = per * sms;
 }
 
+bool ciprng::cta_hist_ok() {
+    static std::mutex mu;
+    static std::map<int, bool> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int resv = -1;
+    if (cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) resv = -1;
+    cudaGetLastError();
+    return cache[dev] = (resv == kCtaHistResvBytes);
+}
+
 static bool env_on(const char *name, bool dflt) {
     const char *v = std::getenv(name);
     if (!v || !v[0]) return dflt;

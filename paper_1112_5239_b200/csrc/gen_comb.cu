@@ -111,8 +111,17 @@ constexpr int comb_fast_min_blocks() {
     return (kLbForceMin1 || (std::is_same<Sink, StoreSink>::value && kCols > 0 && !kStg)) ? 1 : 0;
 }
 
+template <class Sink>
+constexpr int comb_fast_max_threads() {
+    return std::is_same<Sink, StatsSinkCta>::value ? 32 * StatsSinkCta::kWarps : 256;
+}
+template <class Sink, int kCols, bool kStg>
+constexpr int comb_fast_min_blocks_x() {
+    return std::is_same<Sink, StatsSinkCta>::value ? StatsSinkCta::kMinBlocks : comb_fast_min_blocks<Sink, kCols, kStg>();
+}
+
 template <class Src, class Sink, int kCols, bool kStg = false>
-__global__ void __launch_bounds__(256, (comb_fast_min_blocks<Sink, kCols, kStg>())) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__((comb_fast_max_threads<Sink>()), (comb_fast_min_blocks_x<Sink, kCols, kStg>())) comb_fast_kernel(GenArgs a, const __grid_constant__ CUtensorMap tmap) {
     constexpr int X = Src::kPlanes, TP = Src::kPlanes + 1;
     constexpr bool kTma = kCols > 0;
     constexpr uint32_t kTileBytes = kCombTileRows * (kCols > 0 ? kCols : 4) * 4;
@@ -289,6 +298,16 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
         } else if (mode == 0) {
             launch_k(comb_fast_kernel<Src, StoreSink, 0>, dim3(comb_blocks(tiles, 4, 0)), dim3(128), 0, st, a, *tmap);
         } else if (mode == 2) {
+#if !defined(CIPRNG_V3_HIST_WARP)
+            // the CTA histogram (sinks.cuh StatsSinkCta): an invalid half-warp
+            // runs on an all-zero xor64 state and emits zeros, as the sink needs
+            if (cta_hist_ok()) {
+                static_assert(StatsSinkCta::kResv == (uint32_t)kCtaHistResvBytes, "reserved shared memory");
+                launch_cta_hist(comb_fast_kernel<Src, StatsSinkCta, 0>, StatsSinkCta::kWarps,
+                                StatsSinkCta::kSmemBytesExtra, tiles, a.n, st, a, *tmap);
+                return 1;
+            }
+#endif
             auto kern = comb_fast_kernel<Src, StatsSink, 0>;
             const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);

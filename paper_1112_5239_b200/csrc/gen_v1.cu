@@ -95,8 +95,18 @@ constexpr int kFastTileRows = 64;
 // form (device.cuh xor128_f_alu), the store and battery kernels the balanced one
 template <class Sink>
 __device__ __forceinline__ uint32_t v1_x128(uint32_t xk, uint32_t wk3) {
-    if constexpr (std::is_same<Sink, StatsSink>::value) return xor128_f_alu(xk, wk3);
+    if constexpr (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkCta>::value)
+        return xor128_f_alu(xk, wk3);
     else return xor128_f(xk, wk3);
+}
+// the lane's second stream (experiment CIPRNG_CTA_X128B_HI: the CTA-histogram
+// consumer's B stream in the balanced form, w >> 19 on the heavy pipe)
+template <class Sink>
+__device__ __forceinline__ uint32_t v1_x128b(uint32_t xk, uint32_t wk3) {
+#if defined(CIPRNG_CTA_X128B_HI)
+    if constexpr (std::is_same<Sink, StatsSinkCta>::value) return xor128_f(xk, wk3);
+#endif
+    return v1_x128<Sink>(xk, wk3);
 }
 
 
@@ -124,14 +134,17 @@ constexpr int v1_fast_min_blocks() {
 #ifndef CIPRNG_EXP_V1C_MINB
 #define CIPRNG_EXP_V1C_MINB 0
 #endif
+constexpr int kV1CtaWarps = StatsSinkCta::kWarps;
 template <class Sink>
 constexpr int v1_fast_max_threads() {
-    return (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkLane>::value) ? CIPRNG_EXP_V1C_THREADS
-                                                                                              : 256;
+    return std::is_same<Sink, StatsSinkCta>::value ? 32 * kV1CtaWarps
+           : (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkLane>::value) ? CIPRNG_EXP_V1C_THREADS
+                                                                                                : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int v1_fast_min_blocks_x() {
-    return std::is_same<Sink, StatsSink>::value && CIPRNG_EXP_V1C_MINB > 0 ? CIPRNG_EXP_V1C_MINB
+    return std::is_same<Sink, StatsSinkCta>::value                      ? StatsSinkCta::kMinBlocks
+           : std::is_same<Sink, StatsSink>::value && CIPRNG_EXP_V1C_MINB > 0 ? CIPRNG_EXP_V1C_MINB
                                                                             : v1_fast_min_blocks<Sink, kCols, kStg>();
 }
 
@@ -163,6 +176,15 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
     // State of the warp's NEXT tile is loaded into registers while the current
     // one computes (ncu r1e: the first use of freshly loaded state was 18 % of
     // all warp stall samples when every tile waited for its own loads).
+    // Experiment CIPRNG_EXP_V1C_NOPF: consumers load each tile's state when it
+    // starts (their tiles run n >= 2^10 rounds) to save the look-ahead's 12
+    // registers -- per-warp-histogram consumer 77 -> 72 registers, 6 -> 7
+    // CTAs/SM, but 1.849 -> 1.801e12 numbers/s (profiles/experiments/s56); off.
+#if defined(CIPRNG_EXP_V1C_NOPF)
+    constexpr bool kLookAhead = !Sink::kStats;
+#else
+    constexpr bool kLookAhead = true;
+#endif
     uint64_t tile = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     uint32_t pa[6] = {0, 0, 0, 0, 0, 0}, pb[6] = {0, 0, 0, 0, 0, 0};
     const StateIO sio(a);
@@ -174,10 +196,15 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
                 pa[k] = sio.ld(k, sA);
                 pb[k] = sio.ld(k, sB);
             }
+        } else if constexpr (std::is_same<Sink, StatsSinkCta>::value) {
+            // an invalid half-warp runs on an all-zero state (StatsSinkCta::bin)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) pa[k] = pb[k] = 0u;
         }
     };
-    prefetch(tile);
+    if constexpr (kLookAhead) prefetch(tile);
     for (; tile < n_tiles; tile += warps) {
+        if constexpr (!kLookAhead) prefetch(tile);
         const uint64_t row0 = tile * kFastTileRows;
         const bool valid = row0 + 32u * h < a.s_count;  // s_count % 32 == 0
         const uint64_t rA = row0 + rA_t, rB = row0 + rB_t;
@@ -193,7 +220,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
         }
         uint32_t a0 = pa[0], a1 = pa[1], a2 = pa[2], a3 = pa[3], xA = pa[4], tpA = pa[5];
         uint32_t b0 = pb[0], b1 = pb[1], b2 = pb[2], b3 = pb[3], xB = pb[4], tpB = pb[5];
-        prefetch(tile + warps);
+        if constexpr (kLookAhead) prefetch(tile + warps);
         sink.begin_row(0, rA);
         sink.begin_row(1, rB);
         uint32_t u = tpA ^ tpB;  // u[j] = tp[j] ^ tp[j+16]
@@ -201,7 +228,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
 
 #define CIPRNG_V1_ROUND(GA, GA3, GB, GB3, OA, OB)        \
     GA = v1_x128<Sink>(GA, GA3);                              \
-    GB = v1_x128<Sink>(GB, GB3);                              \
+    GB = v1_x128b<Sink>(GB, GB3);                             \
     nb = __shfl_sync(kFull, u, src, 16);                 \
     xA ^= GA ^ nb;                                       \
     xB ^= GB ^ nb;                                       \
@@ -257,7 +284,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
             i = nb4;
             if constexpr (kStg) {
                 for (; i < a.n; ++i) {  // the last n % 4 rounds: scalar stores
-                    uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128<Sink>(b0, b3);
+                    uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128b<Sink>(b0, b3);
                     a0 = a1; a1 = a2; a2 = a3; a3 = gA;
                     b0 = b1; b1 = b2; b2 = b3; b3 = gB;
                     nb = __shfl_sync(kFull, u, src, 16);
@@ -291,7 +318,7 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
             }
 #undef CIPRNG_V1_DIRECT4
             for (; i < a.n; ++i) {  // ragged tail
-                uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128<Sink>(b0, b3);
+                uint32_t gA = v1_x128<Sink>(a0, a3), gB = v1_x128b<Sink>(b0, b3);
                 a0 = a1; a1 = a2; a2 = a3; a3 = gA;
                 b0 = b1; b1 = b2; b2 = b3; b3 = gB;
                 nb = __shfl_sync(kFull, u, src, 16);
@@ -494,6 +521,12 @@ static void launch_fast_tma(const GenArgs &a0, const CUtensorMap &tm, int grid, 
     launch_k(kern, dim3(grid), dim3(32 * wpb), smem, st, a, tm);
 }
 
+static_assert(StatsSinkCta::kResv == (uint32_t)kCtaHistResvBytes, "reserved shared memory assumption");
+static void launch_v1_consume_cta(const GenArgs &a, const CUtensorMap &tm, uint64_t tiles, cudaStream_t st) {
+    launch_cta_hist(v1_fast_kernel<StatsSinkCta, 0>, StatsSinkCta::kWarps, StatsSinkCta::kSmemBytesExtra, tiles, a.n,
+                    st, a, tm);
+}
+
 int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cudaStream_t st,
               const V1Tuning &tune) {
     // mode: 0 store-direct, 1 store-tma, 2 consume, 3 battery, 4 store staged (smem + coalesced STG)
@@ -538,6 +571,16 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
                 const uint64_t needw = (tiles + kW - 1) / kW;
                 launch_k(kern, dim3(persistent_grid(kern, 32 * kW, sm, needw)), dim3(32 * kW), sm, st, a, *tmap);
 #else
+                // default: one conflict-free histogram per CTA (StatsSinkCta);
+                // the per-warp histograms (StatsSink) when the driver's reserved
+                // shared memory is not the 1 KiB the CTA sink's addressing assumes,
+                // or for the comparison build CIPRNG_V1_HIST_WARP
+#if !defined(CIPRNG_V1_HIST_WARP)
+                if (cta_hist_ok()) {
+                    launch_v1_consume_cta(a, *tmap, tiles, st);
+                    return 1;
+                }
+#endif
                 auto kern = v1_fast_kernel<StatsSink, 0>;
                 const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);

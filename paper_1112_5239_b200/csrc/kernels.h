@@ -62,6 +62,11 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 // the unit of the consumer / battery grids (persistent_grid below; sized from
 // the occupancy API because registers limit the consumer to 7 CTAs/SM).
 int resident_blocks(const void *kern, int threads, size_t smem);
+// True when the current device reserves exactly StatsSinkCta::kResv (1 KiB)
+// of shared memory per block, i.e. dynamic shared memory starts at window
+// offset 0x400 as the CTA-histogram consumers' immediate-offset atomics assume.
+constexpr int kCtaHistResvBytes = 1024;
+bool cta_hist_ok();
 // Grid of the consumer / battery kernels: k waves of resident CTAs (k = 0:
 // one tile per warp, no cap; CIPRNG_NVCC_EXTRA=-DCIPRNG_PGRID_WAVES=k for
 // experiments).  Measured (consumers, 2^20 streams, L2 flushed,
@@ -79,6 +84,27 @@ inline int persistent_grid(void (*kern)(KArgs...), int threads, size_t smem, uin
                                                                                  threads, smem);
     const uint64_t b = blocks_needed < (uint64_t)r ? blocks_needed : (uint64_t)r;
     return (int)(b ? b : 1);
+}
+
+// Grid of the CTA-histogram consumers (sinks.cuh StatsSinkCta): k waves of
+// resident CTAs (default 1: 2 x 14 warps per SM take the tiles round-robin),
+// but never so few CTAs that a u32 histogram word could reach 2^31
+// increments -- a word takes at most one increment per round from each warp
+// of its CTA, i.e. tiles-per-warp x warps x n (n < 2^24 host-checked, so one
+// tile per warp always fits).
+#ifndef CIPRNG_V1C_CTA_WAVES
+#define CIPRNG_V1C_CTA_WAVES 1
+#endif
+template <typename... KArgs, typename... Args>
+inline void launch_cta_hist(void (*kern)(KArgs...), int wpb, size_t smem, uint64_t tiles, uint64_t n, cudaStream_t st,
+                            Args &&...args) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device; cheap
+    const uint64_t need = (tiles + wpb - 1) / wpb;
+    uint64_t grid = (uint64_t)CIPRNG_V1C_CTA_WAVES * resident_blocks(reinterpret_cast<const void *>(kern), 32 * wpb, smem);
+    if (grid == 0 || grid > need) grid = need;
+    while (grid < need && ((tiles + grid * wpb - 1) / (grid * wpb)) * (uint64_t)wpb * n >= (1ull << 31)) grid *= 2;
+    if (grid > need) grid = need;
+    launch_k(kern, dim3((unsigned)grid), dim3(32 * wpb), smem, st, std::forward<Args>(args)...);
 }
 
 struct InitArgs {

@@ -367,6 +367,133 @@ struct StatsSinkLane {
     static constexpr bool kStats = true;
 };
 
+// StatsSink with ONE histogram per CTA laid out so that a warp's atomics never
+// share a bank: bin b of column c is the u32 at byte offset 256 b + 4 c of a
+// 64 KiB block, c = lane (the lane's first stream) or 32 + lane (its second).
+// Bank = c mod 32 = lane, so every red.shared is one conflict-free wavefront
+// (StatsSink: ~3.15), and the offset is ONE byte permute -- PRMT puts x's top
+// byte into byte 1 of the lane's column word -- against SHF + IMAD, with the
+// CTA base folded into the atomic's uniform-register operand by ptxas.  All
+// warps of the CTA share the block (same-address atomics from different
+// instructions are still atomic).  No in-kernel flush: the host sizes the
+// grid so that no word can reach 2^31 increments (v1_cta_hist_grid).
+struct StatsSinkCta {
+    uint32_t cols;   // byte 0: 4 * lane, byte 2: 4 * (32 + lane), byte 3: the
+                     // window address' CTA-in-cluster byte; byte 1 zero
+    uint32_t out32;  // outside pairs since the last end_rows
+    uint64_t outside, pairs;
+    uint64_t junk;   // bin-0 increments of this lane's invalid rows (see end_rows)
+    uint32_t pend[2];
+    uint64_t n;
+    static constexpr uint32_t kBytes = 65536;
+    // Dynamic shared memory starts kResv bytes into the CTA's shared window
+    // (the 1 KiB reserved by the driver, cudaDevAttrReservedSharedMemoryPerBlock;
+    // the host checks it before choosing this sink, the ctor traps otherwise),
+    // so the block's address is (cta byte << 24) | kResv and the atomic takes
+    // kResv as its immediate offset: PRMT + ATOMS [R + 0x400], nothing else.
+    static constexpr uint32_t kResv = 1024;
+    static __device__ __forceinline__ uint32_t base() {
+        extern __shared__ __align__(1024) uint8_t smem_dyn[];
+        return smem_u32(smem_dyn);
+    }
+    __device__ __forceinline__ explicit StatsSinkCta(const GenArgs &a)
+        : out32(0), outside(0), pairs(0), junk(0), pend{0, 0}, n(a.n) {
+        const uint32_t lane = threadIdx.x & 31u, b = base();
+        if ((b & 0x00FFFFFFu) != kResv) __trap();
+        cols = (4u * lane) | ((128u + 4u * lane) << 16) | (b & 0xFF000000u);
+        for (uint32_t k = threadIdx.x; k < kBytes / 16u; k += blockDim.x)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(b + 16u * k), "r"(0u) : "memory");
+        __syncthreads();
+    }
+    // Invalid lanes (a half-warp whose 32 rows lie past s_count; s_count % 32
+    // == 0) run the same instructions with an all-zero state, so every number
+    // they emit is 0: they add exactly 2n to bin 0 per tile, which end_rows
+    // books and finish takes back -- no predicate or branch in the round loop.
+#ifndef CIPRNG_CTA_BIN_HI  // experiment: this many of the two slots form the offset on the heavy pipe
+#define CIPRNG_CTA_BIN_HI 0   // (IMAD.HI x >> 24, IMAD bin * 256 + column) instead of one PRMT
+#endif
+    template <int kSlot>
+    __device__ __forceinline__ void bin(uint32_t o) {
+        uint32_t off;  // {column byte, x >> 24, 0, CTA byte}
+        if constexpr (kSlot < CIPRNG_CTA_BIN_HI) {
+            const uint32_t col = kSlot == 0 ? (cols & 0xFF0000FFu) : ((cols >> 16) & 0xFFu) | (cols & 0xFF000000u);
+            asm("{\n\t.reg .u32 b;\n\tmul.hi.u32 b, %1, 256;\n\tmad.lo.u32 %0, b, 256, %2;\n\t}"
+                : "=r"(off) : "r"(o), "r"(col));
+        } else if constexpr (kSlot == 0) asm("prmt.b32 %0, %1, %2, 0x7534;" : "=r"(off) : "r"(o), "r"(cols));
+        else asm("prmt.b32 %0, %1, %2, 0x7536;" : "=r"(off) : "r"(o), "r"(cols));
+        asm volatile("red.shared.add.u32 [%0+1024], 1;" ::"r"(off) : "memory");
+    }
+    __device__ __forceinline__ void pair(uint32_t u, uint32_t v) { count_outside(out32, u, v); }
+    __device__ __forceinline__ void begin_row(int, uint64_t) {}
+    __device__ __forceinline__ void put4(int slot, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
+                                         bool) {
+        if (slot == 0) {
+            bin<0>(o0); bin<0>(o1); bin<0>(o2); bin<0>(o3);
+        } else {
+            bin<1>(o0); bin<1>(o1); bin<1>(o2); bin<1>(o3);
+        }
+        pair(o0, o1);
+        pair(o2, o3);
+    }
+    __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool) {
+        if (slot == 0) bin<0>(o);
+        else bin<1>(o);
+        if (i & 1) pair(pend[slot], o);
+        else pend[slot] = o;
+    }
+    // rows: 2 for a valid lane of the fast kernel, 0 for an invalid one
+    __device__ __forceinline__ void end_rows(uint32_t rows) {
+        outside += rows ? out32 : 0u;
+        junk += rows ? 0u : 2u * n;
+        out32 = 0;
+        pairs += (uint64_t)rows * (n >> 1);
+    }
+    __device__ void finish(const GenArgs &a) {
+        uint64_t v = pairs - outside, p = pairs, jk = junk;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+            v += __shfl_xor_sync(kFull, v, d);
+            p += __shfl_xor_sync(kFull, p, d);
+            jk += __shfl_xor_sync(kFull, jk, d);
+        }
+        __syncthreads();
+        // bin b = sum of its 64 columns; thread b starts at column b (mod 64)
+        // so a warp's 32 loads of one step fall in 32 different banks
+        for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) {
+            uint64_t acc = 0;
+#pragma unroll 8
+            for (uint32_t c = 0; c < 64u; ++c) {
+                uint32_t w;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(base() + 256u * b + 4u * ((c + b) & 63u)));
+                acc += w;
+            }
+            if (acc) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 2 + b), (unsigned long long)acc);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 0), (unsigned long long)v);
+            if (p) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 1), (unsigned long long)p);
+            // the invalid rows' zeros (u64 wrap-around subtraction: the CTA's
+            // own bin-0 total above already holds them)
+            if (jk) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 2), (unsigned long long)(0ull - jk));
+        }
+    }
+    static constexpr int kSmemBytesPerWarp = 0;
+    static constexpr int kSmemBytesExtra = kBytes;
+    static constexpr bool kStats = true;
+    // CTA shape of the kernels that use it: kWarps warps, kMinBlocks CTAs per
+    // SM (2 x 64 KiB of histogram; 2 x 14 warps at <= 72 registers).  28 warps
+    // per SM also divide the C5 shard evenly: 2^14 tiles over 148 x 28 warps
+    // = 3.95 tiles per warp (32 warps: 3.46 -> 4 rounds, 13 % idle).
+#ifndef CIPRNG_V1C_CTA_WARPS
+#define CIPRNG_V1C_CTA_WARPS 14
+#endif
+#ifndef CIPRNG_V1C_CTA_MINB
+#define CIPRNG_V1C_CTA_MINB 2
+#endif
+    static constexpr int kWarps = CIPRNG_V1C_CTA_WARPS;
+    static constexpr int kMinBlocks = CIPRNG_V1C_CTA_MINB;
+};
+
 // Statistical battery counts (reading
 // Q31: a stream's bit sequence within one call is its words in round order,
 // each most significant bit first).  Same state evolution as StatsSink; per

@@ -409,6 +409,27 @@ def test_consume_matches_oracle_stats(variant, S, n):
     assert np.array_equal(g.get_state(), O.state_planes(variant, st))
 
 
+@pytest.mark.parametrize("variant", [W.V1, W.V3])
+@pytest.mark.parametrize("first,S,n", [(32, 32, 4), (96, 2080, 1030), (0, 2**19 + 32, 66)])
+def test_consume_shards_and_tails(variant, first, S, n):
+    """Consumer parity on a shard (s_begin of the global stream space != 0),
+    with a half-warp of invalid rows in the last 64-stream tile (S % 64 = 32),
+    ragged rounds (n % 4 = 2) and, at 2^19 + 32 streams, more tiles than the
+    consumer grid has warps (several tiles per warp through one shared
+    histogram); three calls accumulate into the same stats."""
+    g = P.ChaoticPRNG(SEEDS[1], first + S, variant, shard=(first, S))
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        g.consume(n, stats)
+    st = O.init_states(variant, SEEDS[1], first, S)
+    ref = np.zeros(258, np.uint64)
+    for _ in range(3):
+        O.stats(O.generate(variant, st, n), ref)
+    got = P.as_u64(stats)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+
+
 def test_consume_custom_tables_and_odd_n():
     comb = W.random_comb(W.rng(9), 4, 2)
     g = P.ChaoticPRNG(1, 64, W.V1, comb_size=4, comb=comb)
