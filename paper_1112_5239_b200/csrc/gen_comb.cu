@@ -113,11 +113,11 @@ constexpr int comb_fast_min_blocks() {
 
 template <class Sink>
 constexpr int comb_fast_max_threads() {
-    return std::is_same<Sink, StatsSinkCta>::value ? 32 * StatsSinkCta::kWarps : 256;
+    return Sink::kCtaHist ? 32 * StatsSinkCta::kWarps : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int comb_fast_min_blocks_x() {
-    return std::is_same<Sink, StatsSinkCta>::value ? StatsSinkCta::kMinBlocks : comb_fast_min_blocks<Sink, kCols, kStg>();
+    return Sink::kCtaHist ? StatsSinkCta::kMinBlocks : comb_fast_min_blocks<Sink, kCols, kStg>();
 }
 
 template <class Src, class Sink, int kCols, bool kStg = false>
@@ -312,6 +312,13 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
             const size_t sm = 4 * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);
         } else {
+#if !defined(CIPRNG_BATTERY_HIST_WARP)
+            if (cta_hist_ok()) {
+                launch_cta_hist(comb_fast_kernel<Src, BatterySinkCta, 0>, StatsSinkCta::kWarps,
+                                BatterySinkCta::kSmemBytesExtra, tiles, 4 * a.n, st, a, *tmap);
+                return 1;
+            }
+#endif
             auto kern = comb_fast_kernel<Src, BatterySink, 0>;
             const size_t sm = 4 * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
             launch_k(kern, dim3(persistent_grid(kern, 128, sm, (tiles + 3) / 4)), dim3(128), sm, st, a, *tmap);

@@ -137,13 +137,13 @@ constexpr int v1_fast_min_blocks() {
 constexpr int kV1CtaWarps = StatsSinkCta::kWarps;
 template <class Sink>
 constexpr int v1_fast_max_threads() {
-    return std::is_same<Sink, StatsSinkCta>::value ? 32 * kV1CtaWarps
+    return Sink::kCtaHist ? 32 * kV1CtaWarps
            : (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkLane>::value) ? CIPRNG_EXP_V1C_THREADS
                                                                                                 : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int v1_fast_min_blocks_x() {
-    return std::is_same<Sink, StatsSinkCta>::value                      ? StatsSinkCta::kMinBlocks
+    return Sink::kCtaHist                                                ? StatsSinkCta::kMinBlocks
            : std::is_same<Sink, StatsSink>::value && CIPRNG_EXP_V1C_MINB > 0 ? CIPRNG_EXP_V1C_MINB
                                                                             : v1_fast_min_blocks<Sink, kCols, kStg>();
 }
@@ -558,6 +558,13 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
         } else {
             const uint64_t need = (tiles + 3) / 4;
             if (mode == 3) {
+#if !defined(CIPRNG_BATTERY_HIST_WARP)
+                if (cta_hist_ok()) {  // 4 byte-bin increments per word: the grid bound takes 4n
+                    launch_cta_hist(v1_fast_kernel<BatterySinkCta, 0>, StatsSinkCta::kWarps,
+                                    BatterySinkCta::kSmemBytesExtra, tiles, 4 * a.n, st, a, *tmap);
+                    return 1;
+                }
+#endif
                 auto kern = v1_fast_kernel<BatterySink, 0>;
                 const size_t sm = 4 * BatterySink::kSmemBytesPerWarp + BatterySink::kSmemBytesExtra;
                 launch_k(kern, dim3(persistent_grid(kern, 128, sm, need)), dim3(128), sm, st, a, *tmap);

@@ -48,6 +48,7 @@ struct StoreSink {
     static constexpr int kSmemBytesPerWarp = 0;
     static constexpr int kSmemBytesExtra = 0;
     static constexpr bool kStats = false;
+    static constexpr bool kCtaHist = false;
 };
 
 // Consumer statistics (reading Q24): per-warp 256-bin shared-memory
@@ -249,6 +250,7 @@ struct StatsSink {
     static constexpr int kSmemBytesPerWarp = 1024;
     static constexpr int kSmemBytesExtra = 1024;  // the discard bins
     static constexpr bool kStats = true;
+    static constexpr bool kCtaHist = false;
 };
 
 // StatsSink with a PRIVATE histogram column per lane (experiment
@@ -365,6 +367,7 @@ struct StatsSinkLane {
     static constexpr int kSmemBytesPerWarp = kWordsPerWarp * 4;
     static constexpr int kSmemBytesExtra = 2048;
     static constexpr bool kStats = true;
+    static constexpr bool kCtaHist = false;
 };
 
 // StatsSink with ONE histogram per CTA laid out so that a warp's atomics never
@@ -480,6 +483,7 @@ struct StatsSinkCta {
     static constexpr int kSmemBytesPerWarp = 0;
     static constexpr int kSmemBytesExtra = kBytes;
     static constexpr bool kStats = true;
+    static constexpr bool kCtaHist = true;
     // CTA shape of the kernels that use it: kWarps warps, kMinBlocks CTAs per
     // SM (2 x 64 KiB of histogram; 2 x 14 warps at <= 72 registers).  28 warps
     // per SM also divide the C5 shard evenly: 2^14 tiles over 148 x 28 warps
@@ -505,29 +509,54 @@ struct StatsSinkCta {
 //   stream; and a per-warp shared histogram of all four bytes of every word.
 // stats layout (264 u64): [0] ones [1] diff [2] c11 [3] lag8 [4] block_sq
 // [5] blocks [6] first ones [7] last ones [8 + b] byte b.
-struct BatterySink {
+// kCta = false: per-warp 256-bin histograms (3.15 bank-conflicted wavefronts
+// per atomic; the L1/shared data pipe binds, ncu r2e 0.81).  kCta = true: the
+// conflict-free CTA layout of StatsSinkCta (byte k of x lands in byte 1 of the
+// lane's column word by one PRMT, selector 0x75k4 / 0x75k6), no in-kernel
+// flush (the host sizes the grid for 4 increments per word, launch_cta_hist).
+template <bool kCta>
+struct BatterySinkT {
     static constexpr int kWords = 264;
-    uint32_t hist;           // shared address of this warp's 256 u32 bins
+    uint32_t hist;           // per-warp: shared address of this warp's 256 u32 bins; CTA: the column word
     uint32_t ones, diff, c11, lag8, bsq;
     uint64_t acc[8];
     uint32_t prev[2];
     uint64_t n;
     uint64_t pending;
     uint64_t *gstats;
-    __device__ __forceinline__ explicit BatterySink(const GenArgs &a)
+    __device__ __forceinline__ explicit BatterySinkT(const GenArgs &a)
         : ones(0), diff(0), c11(0), lag8(0), bsq(0), acc{0, 0, 0, 0, 0, 0, 0, 0}, prev{0, 0}, n(a.n), pending(0),
           gstats(a.stats) {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
-        uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
-        for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
+        if constexpr (kCta) {
+            const uint32_t lane = threadIdx.x & 31u, b = StatsSinkCta::base();
+            if ((b & 0x00FFFFFFu) != StatsSinkCta::kResv) __trap();
+            hist = (4u * lane) | ((128u + 4u * lane) << 16) | (b & 0xFF000000u);
+            for (uint32_t k = threadIdx.x; k < StatsSinkCta::kBytes / 16u; k += blockDim.x)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(b + 16u * k), "r"(0u) : "memory");
+        } else {
+            uint32_t *all = reinterpret_cast<uint32_t *>(smem_dyn);
+            for (uint32_t k = threadIdx.x; k < 256u * (blockDim.x >> 5); k += blockDim.x) all[k] = 0;
+            hist = smem_u32(all) + 1024u * (threadIdx.x >> 5);
+        }
         __syncthreads();
-        hist = smem_u32(all) + 1024u * (threadIdx.x >> 5);
     }
-    __device__ __forceinline__ void bin(uint32_t b) {
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist + 4u * b) : "memory");
+    // byte kByte of x into the histogram (slot: the lane's stream, CTA layout only)
+    template <int kByte>
+    __device__ __forceinline__ void bin(int slot, uint32_t x) {
+        if constexpr (kCta) {
+            constexpr uint32_t selA = 0x7504u | (kByte << 4), selB = 0x7506u | (kByte << 4);
+            uint32_t off;
+            if (slot == 0) asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(x), "r"(hist), "n"(selA));
+            else asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(x), "r"(hist), "n"(selB));
+            asm volatile("red.shared.add.u32 [%0+1024], 1;" ::"r"(off) : "memory");
+        } else {
+            const uint32_t b = kByte == 3 ? (x >> 24) : ((x >> (8 * kByte)) & 0xFFu);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist + 4u * b) : "memory");
+        }
     }
     // one word x of a stream whose previous word in this call is p (has_prev)
-    __device__ __forceinline__ void word(uint32_t x, uint32_t p, bool has_prev) {
+    __device__ __forceinline__ void word(int slot, uint32_t x, uint32_t p, bool has_prev) {
         ones += __popc(x);
         diff += __popc((x ^ (x >> 1)) & 0x7FFFFFFFu);
         c11 += __popc(x & (x >> 1));
@@ -537,20 +566,20 @@ struct BatterySink {
             c11 += p & (x >> 31) & 1u;
             lag8 += __popc((p ^ (x >> 24)) & 0xFFu);
         }
-        bin(x & 0xFFu);
-        bin((x >> 8) & 0xFFu);
-        bin((x >> 16) & 0xFFu);
-        bin(x >> 24);
+        bin<0>(slot, x);
+        bin<1>(slot, x);
+        bin<2>(slot, x);
+        bin<3>(slot, x);
     }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int slot, uint64_t i, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool valid) {
         if (!valid) return;
         if (i == 0) acc[6] += o0 >> 31;
-        word(o0, prev[slot], i != 0);
-        word(o1, o0, true);
-        word(o2, o1, true);
-        word(o3, o2, true);
+        word(slot, o0, prev[slot], i != 0);
+        word(slot, o1, o0, true);
+        word(slot, o2, o1, true);
+        word(slot, o3, o2, true);
         const int c = (int)(__popc(o0) + __popc(o1) + __popc(o2) + __popc(o3)) - 64;
         bsq += (uint32_t)(c * c);
         prev[slot] = o3;
@@ -558,7 +587,7 @@ struct BatterySink {
     __device__ __forceinline__ void put1(int slot, uint64_t i, uint32_t o, bool valid) {
         if (!valid) return;
         if (i == 0) acc[6] += o >> 31;
-        word(o, prev[slot], i != 0);
+        word(slot, o, prev[slot], i != 0);
         prev[slot] = o;
     }
     __device__ __forceinline__ void end_rows(uint32_t rows) {
@@ -567,10 +596,12 @@ struct BatterySink {
         acc[5] += (uint64_t)rows * (n >> 2);
         if (rows >= 1) acc[7] += prev[0] & 1u;
         if (rows >= 2) acc[7] += prev[1] & 1u;
-        pending += 4 * kMaxRowsPerWarpTile * n;
-        if (pending + 4 * kMaxRowsPerWarpTile * n >= kHistFlushAt) {  // warp-uniform
-            warp_hist_flush(hist, gstats + 8);
-            pending = 0;
+        if constexpr (!kCta) {
+            pending += 4 * kMaxRowsPerWarpTile * n;
+            if (pending + 4 * kMaxRowsPerWarpTile * n >= kHistFlushAt) {  // warp-uniform
+                warp_hist_flush(hist, gstats + 8);
+                pending = 0;
+            }
         }
     }
     __device__ void finish(const GenArgs &a) {
@@ -587,7 +618,12 @@ struct BatterySink {
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < 256u; b += blockDim.x) {
             uint64_t s = 0;
-            for (uint32_t w = 0; w < nw; ++w) s += all[256u * w + b];
+            if constexpr (kCta) {
+#pragma unroll 8
+                for (uint32_t c = 0; c < 64u; ++c) s += all[64u * b + ((c + b) & 63u)];
+            } else {
+                for (uint32_t w = 0; w < nw; ++w) s += all[256u * w + b];
+            }
             if (s) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + 8 + b), (unsigned long long)s);
         }
         if ((threadIdx.x & 31) == 0) {
@@ -596,9 +632,12 @@ struct BatterySink {
                 if (acc[k]) atomicAdd(reinterpret_cast<unsigned long long *>(a.stats + k), (unsigned long long)acc[k]);
         }
     }
-    static constexpr int kSmemBytesPerWarp = 1024;
-    static constexpr int kSmemBytesExtra = 0;
+    static constexpr int kSmemBytesPerWarp = kCta ? 0 : 1024;
+    static constexpr int kSmemBytesExtra = kCta ? (int)StatsSinkCta::kBytes : 0;
     static constexpr bool kStats = true;
+    static constexpr bool kCtaHist = kCta;
 };
+using BatterySink = BatterySinkT<false>;
+using BatterySinkCta = BatterySinkT<true>;
 
 }  // namespace ciprng

@@ -601,6 +601,22 @@ def test_battery_matches_oracle_counts(variant, S, n):
         g.battery(2**20)
 
 
+@pytest.mark.parametrize("variant", [W.V1, W.V3])
+def test_battery_shard_multi_tile(variant):
+    """The battery's CTA histogram (V1 / V3 fast kernels) over more tiles than
+    the grid has warps, on a shard whose last tile holds an invalid half-warp,
+    with a ragged round count."""
+    first, S, n = 64, 2**19 + 32, 34
+    g = P.ChaoticPRNG(SEEDS[2], first + S, variant, shard=(first, S))
+    stats = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    g.battery(n, stats)
+    st = O.init_states(variant, SEEDS[2], first, S)
+    ref = O.battery(O.generate(variant, st, n), np.zeros(O.N_BATTERY, np.uint64))
+    got = P.as_u64(stats)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("variant", [W.V0, W.V1, W.V2, W.V3, W.V4])
 def test_battery_1e10_numbers(variant):

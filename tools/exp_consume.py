@@ -31,4 +31,19 @@ for var in (P.V1, P.V3, P.V2, P.V0):
     ms = sum(a.elapsed_time(b) for a, b in ev) / K
     res[f"v{var}_consume"] = S * nn / (ms / 1e3)
     g.close()
+for var in (P.V1, P.V3):  # the NEXT-2 battery (same shape)
+    g = P.ChaoticPRNG(1, S, var)
+    bst = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        g.battery(n, bst)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        fl(k)
+        ev[k][0].record(st)
+        g.battery(n, bst)
+        ev[k][1].record(st)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    res[f"v{var}_battery"] = S * n / (ms / 1e3)
+    g.close()
 print(json.dumps(res))
