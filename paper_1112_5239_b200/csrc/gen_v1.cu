@@ -311,6 +311,10 @@ __global__ void __launch_bounds__((v1_fast_max_threads<Sink>()), (v1_fast_min_bl
                 // consumers: n < 2^24 (host-checked), a 32-bit trip counter
                 // and index (the u64 loop against a.n cost 8 instructions per 4 rounds)
                 const uint32_t n4 = (uint32_t)a.n & ~3u;
+#if defined(CIPRNG_EXP_V1C_UNROLL)  // experiment: unroll the 4-round body further
+                constexpr int kUnroll = CIPRNG_EXP_V1C_UNROLL;
+#pragma unroll kUnroll
+#endif
                 for (uint32_t i32 = 0; i32 != n4; i32 += 4) CIPRNG_V1_DIRECT4(i32)
                 i = n4;
             } else {

@@ -401,6 +401,7 @@ struct StatsSinkCta {
     }
     __device__ __forceinline__ explicit StatsSinkCta(const GenArgs &a)
         : out32(0), outside(0), pairs(0), junk(0), pend{0, 0}, n(a.n) {
+        zero = a.zero;
         const uint32_t lane = threadIdx.x & 31u, b = base();
         if ((b & 0x00FFFFFFu) != kResv) __trap();
         cols = (4u * lane) | ((128u + 4u * lane) << 16) | (b & 0xFF000000u);
@@ -426,7 +427,14 @@ struct StatsSinkCta {
         else asm("prmt.b32 %0, %1, %2, 0x7536;" : "=r"(off) : "r"(o), "r"(cols));
         asm volatile("red.shared.add.u32 [%0+1024], 1;" ::"r"(off) : "memory");
     }
-    __device__ __forceinline__ void pair(uint32_t u, uint32_t v) { count_outside(out32, u, v); }
+    uint32_t zero = 0;  // GenArgs::zero (experiment CIPRNG_EXP_CTA_MADC)
+    __device__ __forceinline__ void pair(uint32_t u, uint32_t v) {
+#if defined(CIPRNG_EXP_CTA_MADC)  // the counter's add-with-carry on the heavy pipe (IMAD.X)
+        count_outside_madc(out32, u, v, zero);
+#else
+        count_outside(out32, u, v);
+#endif
+    }
     __device__ __forceinline__ void begin_row(int, uint64_t) {}
     __device__ __forceinline__ void put4(int slot, uint64_t, uint32_t o0, uint32_t o1, uint32_t o2, uint32_t o3,
                                          bool) {
