@@ -648,6 +648,20 @@ def run_ours(args):
     return 0
 
 
+def _hist_chi2(hist) -> dict:
+    """SURVEY s8(d) C5 "chi^2_255 sane": Pearson chi^2 of the 256-bin top-byte
+    histogram against uniform (host-side float on the final integer counts)
+    and its upper-tail p-value (scipy's chi2 survival function)."""
+    from scipy.stats import chi2
+
+    h = [int(v) for v in hist]
+    tot = sum(h)
+    e = tot / 256.0
+    x2 = sum((v - e) ** 2 for v in h) / e
+    p = float(chi2.sf(x2, 255))
+    return {"hist_chi2_255": x2, "hist_chi2_p": p, "hist_chi2_sane": 1e-6 < p < 1 - 1e-6}
+
+
 def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
     """C5 (BASELINE configs[4]) as a job over every rank: V1 consumer mode on
     a global stream space of 2^20 streams per GPU (rank r owns the contiguous
@@ -703,6 +717,7 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
             "pairs_exact": pairs == steps * S * ws * n // 2,
             "hist_total_exact": int(st[2:].sum()) == steps * S * ws * n,
             "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma,
+            **_hist_chi2(st[2:]),
             "verify": {"streams": c5["n_streams"], "n": c5["n"], "calls": 1,
                        "stats_sha256": vsha, "note": "fixed global stream space; identical at every GPU count"}}
 
@@ -891,7 +906,9 @@ def measure_secondary(P, torch, dev, args):
     g = P.ChaoticPRNG(W.SEEDS[0], S5, P.V1)
     stats = torch.zeros(P.N_STATS, dtype=torch.int64, device=dev)
     s = timed(lambda: g.consume(n5, stats), 10)
-    res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5}
+    st5 = P.as_u64(stats)
+    res["c5_v1_consume"] = {"value": S5 * n5 / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S5, "n": n5,
+                            "pi_hat": 4 * int(st5[0]) / int(st5[1]), **_hist_chi2(st5[2:])}
     g.close()
     # the other variants in consumer mode (SURVEY s8(d) C5 "also V0 and V2"):
     # the like-for-like rows for the paper's no-store figures -- V3 is its
