@@ -849,6 +849,48 @@ def measure_c4_sharded(P, torch, dev):
             "digest_list_sha256": hashlib.sha256(dl.tobytes()).hexdigest()}
 
 
+def measure_curand(torch, dev, timed) -> dict:
+    """Same-box context ("cuRAND ... not a target"): NVIDIA's
+    library generators filling the C2-sized buffer (2^27 u32 = 512 MiB per
+    call, curandGenerate) with the secondary rows' timing (L2 flushed before
+    every call, CUDA events).  A LIBRARY on this box, not part of the path:
+    the V1 row to set it against is `v1_c2_same_timing` (the headline kernel
+    through the same helper)."""
+    import ctypes
+
+    lib = None
+    for name in ("libcurand.so.10", "/usr/local/cuda/lib64/libcurand.so"):
+        try:
+            lib = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    if lib is None:
+        return {"unavailable": "libcurand not found"}
+    words = 2**27
+    out = torch.empty(words, dtype=torch.int32, device=dev)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rows = {}
+    for name, rng in (("XORWOW", 101), ("PHILOX4_32_10", 161), ("MRG32K3A", 121), ("MTGP32", 141)):
+        g = ctypes.c_void_p()
+        if lib.curandCreateGenerator(ctypes.byref(g), rng) != 0:
+            rows[name] = {"unavailable": "curandCreateGenerator failed"}
+            continue
+        lib.curandSetStream(g, st)
+        lib.curandSetPseudoRandomGeneratorSeed(g, ctypes.c_ulonglong(W.SEEDS[0]))
+        ptr = ctypes.c_void_p(out.data_ptr())
+
+        def call():
+            if lib.curandGenerate(g, ptr, ctypes.c_size_t(words)) != 0:
+                raise RuntimeError(f"curandGenerate({name}) failed")
+
+        s = timed(call, 20)
+        rows[name] = {"value": words / s, "unit": UNIT, "ms_per_call": s * 1e3, "write_gbs": words * 4 / s / 1e9}
+        lib.curandDestroyGenerator(g)
+    del out
+    return {"kind": "library context (not a target, not our path)", "words_per_call": words, "generators": rows}
+
+
 def measure_secondary(P, torch, dev, args):
     """Other rows of SURVEY s8(a) on this GPU (not the headline): V2 store
     (C3), V0 store and V1 fused consumer; numbers/s with CUDA events."""
@@ -961,6 +1003,16 @@ def measure_secondary(P, torch, dev, args):
     s = timed(lambda: CH.alg1_generate(32, 8, za, xa, na), 10)
     res["alg1_negation_b8"] = {"value": Sa * na / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": Sa,
                                "n": na, "cells": 32, "b": 8}
+    # the headline kernel through the same helper (flushed, not charged) for the cuRAND comparison
+    S2, n2 = W.CONFIGS["C2"]["n_streams"], W.CONFIGS["C2"]["n"]
+    g = P.ChaoticPRNG(W.SEEDS[0], S2, P.V1)
+    out = torch.empty((S2, n2), dtype=torch.int32, device=dev)
+    s = timed(lambda: g.generate(n2, out=out), 20)
+    res["v1_c2_same_timing"] = {"value": S2 * n2 / s, "unit": UNIT, "ms_per_call": s * 1e3,
+                                "note": "event-timed, L2 flushed before each call, deferred write-back not charged"}
+    g.close()
+    del out
+    res["curand_context"] = measure_curand(torch, dev, timed)
     # last: the 10^12-number job runs the GPU hot for seconds (power cap),
     # which slowed the row measured right after it by up to 13 % (r2b battery)
     res["c4_sharded_1e12"] = measure_c4_sharded(P, torch, dev)
