@@ -177,7 +177,14 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
                   cudaStream_t st, int grid);
 // v0_jump.cu: one V0 stream split over the GPU by GF(2) jump-ahead + XOR
 // scan (C1).  The plan (jump polynomials for one (L, B)) lives in the handle.
-constexpr int kJumpThreads = 128;  // 256: 34.8 vs 28.8 us per C1 call (more sweeps per SM)
+#ifndef CIPRNG_JUMP_THREADS  // experiment knob
+#define CIPRNG_JUMP_THREADS 128
+#endif
+// 128 threads per CTA: 25.2 us per C1 call; 256: 26.6 us (profiles/experiments/s62;
+// bit-sweep era 34.8 vs 28.8).  Fewer than 128 is not supported (64 produced
+// wrong words in s62: the kernel's per-CTA setup assumes at least 4 warps).
+constexpr int kJumpThreads = CIPRNG_JUMP_THREADS;
+static_assert(kJumpThreads >= 128 && kJumpThreads % 32 == 0, "v0_jump_kernel needs >= 4 warps per CTA");
 constexpr int kJumpPolyWords = 6;
 constexpr int kJumpMaxDeg[3] = {64, 256, 320};  // state bits of xor64, xor128-64, xorwow-64
 constexpr uint32_t kJumpMaxL = 64;              // rounds per segment (shared-memory staging)
