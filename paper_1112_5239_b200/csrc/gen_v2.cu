@@ -133,11 +133,23 @@ __device__ __forceinline__ uint32_t v2_strategy(Bbs8 &b) {
 // minimum is set for an experiment.
 template <class Sink>
 constexpr int v2_min_blocks() {
-    return CIPRNG_V2_MINB > 1 ? CIPRNG_V2_MINB : (std::is_same<Sink, StatsSink>::value ? 1 : 0);
+    return CIPRNG_V2_MINB > 1 ? CIPRNG_V2_MINB
+                              : ((std::is_same<Sink, StatsSink>::value || Sink::kCtaHist) ? 1 : 0);
+}
+// Experiment CIPRNG_V2_HIST_CTA: the CTA-histogram consumer (sinks.cuh
+// StatsSinkCta1), one CTA of kV2CtaWarps warps per SM sharing the 64 KiB
+// conflict-free histogram (slower, see launch_v2).
+#ifndef CIPRNG_V2C_CTA_WARPS
+#define CIPRNG_V2C_CTA_WARPS 21
+#endif
+constexpr int kV2CtaWarps = CIPRNG_V2C_CTA_WARPS;
+template <class Sink>
+constexpr int v2_max_threads() {
+    return Sink::kCtaHist ? 32 * kV2CtaWarps : 32 * CIPRNG_V2_WPB;
 }
 
 template <class Sink, uint32_t kFMask, bool kPack>
-__global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, v2_min_blocks<Sink>()) v2_kernel(GenArgs a) {
+__global__ void __launch_bounds__(v2_max_threads<Sink>(), v2_min_blocks<Sink>()) v2_kernel(GenArgs a) {
     Sink sink(a);
     pdl_launch_dependents();
     pdl_wait();  // previous grid on the stream complete + visible
@@ -181,8 +193,11 @@ __global__ void __launch_bounds__(32 * CIPRNG_V2_WPB, v2_min_blocks<Sink>()) v2_
             }
         }
         if (!valid) {
+            // the CTA histogram needs an invalid lane to emit zeros: y = 0
+            // squares to 0, so every nibble, shift and filler is 0 (its
+            // combination group is all invalid: s_count % C == 0)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) b.y[j] = 2u;
+            for (int j = 0; j < 8; ++j) b.y[j] = Sink::kCtaHist ? 0u : 2u;
             x = tp = 0;
         }
         if constexpr (kFMask == kMontMask) {
@@ -273,6 +288,19 @@ int launch_v2(const GenArgs &a, int mode, cudaStream_t st, int kind) {
     const int wpb = CIPRNG_V2_WPB;
     uint64_t blocks = (tiles + wpb - 1) / wpb;
     if (mode == 2) {
+        // The CTA histogram (StatsSinkCta1) measured SLOWER here than the
+        // per-warp one (C5 shape, n = 1024: 2.54 / 2.84 / 2.94e11 at 21 / 24 /
+        // 16 warps per CTA against 2.99e11; profiles/experiments/s63-s64) --
+        // the heavy-pipe bound V2 consumer gains nothing from the freed IMAD
+        // and loses ILP at the lower register budget.  Kept as an experiment.
+#if defined(CIPRNG_V2_HIST_CTA)
+        if (cta_hist_ok()) {
+            static_assert(StatsSinkCta1::kResv == (uint32_t)kCtaHistResvBytes, "reserved shared memory");
+            launch_cta_hist(v2_kernel<StatsSinkCta1, kV2FMask, kV2Pack>, kV2CtaWarps, StatsSinkCta1::kSmemBytesExtra,
+                            tiles, a.n, st, a);
+            return 1;
+        }
+#endif
         auto kern = v2_kernel<StatsSink, kV2FMask, kV2Pack>;
         const size_t sm = wpb * StatsSink::kSmemBytesPerWarp + StatsSink::kSmemBytesExtra;
         launch_k(kern, dim3(persistent_grid(kern, 32 * wpb, sm, blocks)), dim3(32 * wpb), sm, st, a);

@@ -380,7 +380,10 @@ struct StatsSinkLane {
 // warps of the CTA share the block (same-address atomics from different
 // instructions are still atomic).  No in-kernel flush: the host sizes the
 // grid so that no word can reach 2^31 increments (v1_cta_hist_grid).
-struct StatsSinkCta {
+// kLaneStreams: streams per lane of the kernel using it (2: the V1 / V3 fast
+// kernels' lanes own rows j and j + 16; 1: one stream per lane, V2)
+template <int kLaneStreams>
+struct StatsSinkCtaT {
     uint32_t cols;   // byte 0: 4 * lane, byte 2: 4 * (32 + lane), byte 3: the
                      // window address' CTA-in-cluster byte; byte 1 zero
     uint32_t out32;  // outside pairs since the last end_rows
@@ -399,7 +402,7 @@ struct StatsSinkCta {
         extern __shared__ __align__(1024) uint8_t smem_dyn[];
         return smem_u32(smem_dyn);
     }
-    __device__ __forceinline__ explicit StatsSinkCta(const GenArgs &a)
+    __device__ __forceinline__ explicit StatsSinkCtaT(const GenArgs &a)
         : out32(0), outside(0), pairs(0), junk(0), pend{0, 0}, n(a.n) {
         zero = a.zero;
         const uint32_t lane = threadIdx.x & 31u, b = base();
@@ -409,10 +412,11 @@ struct StatsSinkCta {
             asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(b + 16u * k), "r"(0u) : "memory");
         __syncthreads();
     }
-    // Invalid lanes (a half-warp whose 32 rows lie past s_count; s_count % 32
-    // == 0) run the same instructions with an all-zero state, so every number
-    // they emit is 0: they add exactly 2n to bin 0 per tile, which end_rows
-    // books and finish takes back -- no predicate or branch in the round loop.
+    // Invalid lanes (rows past s_count: a half-warp of the fast kernels, whole
+    // combination groups of V2) run the same instructions with an all-zero
+    // state, so every number they emit is 0: they add exactly n per stream
+    // slot to bin 0 per tile, which end_rows books and finish takes back -- no
+    // predicate or branch in the round loop.
 #ifndef CIPRNG_CTA_BIN_HI  // experiment: this many of the two slots form the offset on the heavy pipe
 #define CIPRNG_CTA_BIN_HI 0   // (IMAD.HI x >> 24, IMAD bin * 256 + column) instead of one PRMT
 #endif
@@ -452,10 +456,10 @@ struct StatsSinkCta {
         if (i & 1) pair(pend[slot], o);
         else pend[slot] = o;
     }
-    // rows: 2 for a valid lane of the fast kernel, 0 for an invalid one
+    // rows: kLaneStreams for a valid lane, 0 for an invalid one
     __device__ __forceinline__ void end_rows(uint32_t rows) {
         outside += rows ? out32 : 0u;
-        junk += rows ? 0u : 2u * n;
+        junk += rows ? 0u : (uint64_t)kLaneStreams * n;
         out32 = 0;
         pairs += (uint64_t)rows * (n >> 1);
     }
@@ -505,6 +509,8 @@ struct StatsSinkCta {
     static constexpr int kWarps = CIPRNG_V1C_CTA_WARPS;
     static constexpr int kMinBlocks = CIPRNG_V1C_CTA_MINB;
 };
+using StatsSinkCta = StatsSinkCtaT<2>;
+using StatsSinkCta1 = StatsSinkCtaT<1>;
 
 // Statistical battery counts (reading
 // Q31: a stream's bit sequence within one call is its words in round order,

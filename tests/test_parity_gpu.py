@@ -409,14 +409,16 @@ def test_consume_matches_oracle_stats(variant, S, n):
     assert np.array_equal(g.get_state(), O.state_planes(variant, st))
 
 
-@pytest.mark.parametrize("variant", [W.V1, W.V3])
-@pytest.mark.parametrize("first,S,n", [(32, 32, 4), (96, 2080, 1030), (0, 2**19 + 32, 66)])
+@pytest.mark.parametrize("variant,first,S,n", [
+    (v, *c) for v in (W.V1, W.V3) for c in ((32, 32, 4), (96, 2080, 1030), (0, 2**19 + 32, 66))
+] + [(W.V2, 32, 32, 4), (W.V2, 96, 2080, 1030), (W.V2, 0, 2**17 + 32, 34)])
 def test_consume_shards_and_tails(variant, first, S, n):
     """Consumer parity on a shard (s_begin of the global stream space != 0),
-    with a half-warp of invalid rows in the last 64-stream tile (S % 64 = 32),
-    ragged rounds (n % 4 = 2) and, at 2^19 + 32 streams, more tiles than the
-    consumer grid has warps (several tiles per warp through one shared
-    histogram); three calls accumulate into the same stats."""
+    with invalid rows in the last tile (V1 / V3: a half-warp, S % 64 = 32;
+    V2's 32-stream tiles are whole), ragged rounds (n % 4 = 2) and, at
+    2^19 + 32 (V2: 2^17 + 32) streams, more tiles than the consumer grid has
+    warps (several tiles per warp through one CTA histogram); three calls
+    accumulate into the same stats."""
     g = P.ChaoticPRNG(SEEDS[1], first + S, variant, shard=(first, S))
     stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
     for _ in range(3):
@@ -428,6 +430,26 @@ def test_consume_shards_and_tails(variant, first, S, n):
     got = P.as_u64(stats)
     assert np.array_equal(got, ref), first_mismatch(got, ref)
     assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+
+
+@pytest.mark.parametrize("C,S", [(4, 100), (8, 200), (32, 64)])
+def test_v2_consume_custom_tables_partial_warp(C, S):
+    """V2 consumer with custom combination arrays and S % 32 != 0: the last
+    warp holds valid lanes and invalid ones (whole combination groups of C
+    streams), the invalid lanes running on y = 0 (the CTA histogram's
+    zero-emitting lanes); stats and state equal the oracle's over 2 calls."""
+    comb = W.random_comb(W.rng(40 + C), C, 16)
+    g = P.ChaoticPRNG(SEEDS[1], S, W.V2, comb_size=C, comb=comb)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    for n in (66, 6):
+        g.consume(n, stats)
+    st = O.init_states(W.V2, SEEDS[1], 0, S)
+    ref = np.zeros(258, np.uint64)
+    for n in (66, 6):
+        O.stats(O.generate(W.V2, st, n, comb_size=C, comb=comb), ref)
+    got = P.as_u64(stats)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), O.state_planes(W.V2, st))
 
 
 def test_consume_custom_tables_and_odd_n():

@@ -30,6 +30,17 @@ for var in (P.V1, P.V3, P.V2, P.V0):
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev) / K
     res[f"v{var}_consume"] = S * nn / (ms / 1e3)
+    if var == P.V2:  # also at the bench's C5 shape (n = 1024)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+        g.consume(n, stats)
+        for k in range(5):
+            fl(k)
+            ev[k][0].record(st)
+            g.consume(n, stats)
+            ev[k][1].record(st)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / 5
+        res["v2_consume_1024"] = S * n / (ms / 1e3)
     g.close()
 for var in (P.V1, P.V3):  # the NEXT-2 battery (same shape)
     g = P.ChaoticPRNG(1, S, var)
