@@ -202,7 +202,12 @@ CIPRNG_API int prng_emit(prng_t *h, uint64_t n_per_stream, int fd, int format, u
  *   [1] number of pairs = n_local * n / 2;
  *   [2 + b] count of x with x >> 24 == b, b = 0..255.
  * Integer sums, so results are independent of launch shape and of how
- * streams are sharded (the multi-GPU all-reduce is bit-exact).
+ * streams are sharded (the multi-GPU all-reduce is bit-exact).  Launch:
+ * V1 / V3 with the default arrays run 14-warp CTAs with one 64 KiB
+ * histogram each (dynamic shared memory, set per call with
+ * cudaFuncSetAttribute on the current device), other kernels per-warp 1 KiB
+ * histograms; the V1 / V3 kernels fall back to the per-warp form when the
+ * device's reserved shared memory per block is not 1 KiB.
  * Errors: PRNG_EINVAL if n is odd or a pointer is NULL, PRNG_ESIZE if
  * n >= 2^24 (split the call; V0/V1/V3/V4 are split invariant), PRNG_ECUDA. */
 CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
