@@ -127,6 +127,8 @@ int ciprng::resident_blocks(const void *kern, int threads, size_t smem) {
     return cache[key] = per * sms;
 }
 
+static bool env_on(const char *name, bool dflt);
+
 bool ciprng::cta_hist_ok() {
     static std::mutex mu;
     static std::map<int, bool> cache;
@@ -138,7 +140,8 @@ bool ciprng::cta_hist_ok() {
     int resv = -1;
     if (cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) resv = -1;
     cudaGetLastError();
-    return cache[dev] = (resv == kCtaHistResvBytes);
+    // CIPRNG_CTA_HIST=0 forces the per-warp histograms (tests of the fallback)
+    return cache[dev] = (resv == kCtaHistResvBytes) && env_on("CIPRNG_CTA_HIST", true);
 }
 
 static bool env_on(const char *name, bool dflt) {

@@ -432,6 +432,38 @@ def test_consume_shards_and_tails(variant, first, S, n):
     assert np.array_equal(g.get_state(), O.state_planes(variant, st))
 
 
+def test_consume_battery_per_warp_fallback():
+    """CIPRNG_CTA_HIST=0 (as on a device whose reserved shared memory per
+    block is not 1 KiB): the V1 / V3 consumers and battery take the per-warp
+    histograms instead of the CTA one; counters still equal the oracle's."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json, sys, numpy as np, torch; sys.path.insert(0, '.')\n"
+        "import paper_1112_5239_b200 as P, workloads as W\n"
+        "out = {}\n"
+        "for v in (W.V1, W.V3):\n"
+        "    g = P.ChaoticPRNG(W.SEEDS[0], 2080, v)\n"
+        "    s = torch.zeros(P.N_STATS, dtype=torch.int64, device='cuda'); g.consume(130, s)\n"
+        "    b = torch.zeros(P.N_BATTERY, dtype=torch.int64, device='cuda'); g.battery(34, b)\n"
+        "    out[v] = [P.as_u64(s).tolist(), P.as_u64(b).tolist()]\n"
+        "print(json.dumps(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=root,
+                       env={**os.environ, "CIPRNG_CTA_HIST": "0"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for v in (W.V1, W.V3):
+        st = O.init_states(v, SEEDS[0], 0, 2080)
+        ref_s = O.stats(O.generate(v, st, 130))
+        ref_b = O.battery(O.generate(v, st, 34))
+        assert np.array_equal(np.array(got[str(v)][0], np.uint64), ref_s)
+        assert np.array_equal(np.array(got[str(v)][1], np.uint64), ref_b)
+
+
 @pytest.mark.parametrize("C,S", [(4, 100), (8, 200), (32, 64)])
 def test_v2_consume_custom_tables_partial_warp(C, S):
     """V2 consumer with custom combination arrays and S % 32 != 0: the last
