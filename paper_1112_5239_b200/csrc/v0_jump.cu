@@ -339,8 +339,44 @@ constexpr size_t kTabWords = (size_t)16 * (kTab1 * 1 + kTab2 * 4 + kTab3 * 5);
 // XOR of at most four window words (broadcast loads: neighbouring threads
 // share the chunk) -- so a warp's stores cover 256 contiguous bytes.
 template <int W>
+__device__ __forceinline__ void pair_vals(const uint64_t *w, uint32_t e2, uint64_t &even, uint64_t &odd) {
+    const uint32_t ck = e2 >> 3, p0 = (e2 & 7u) * 2;  // (chunk, word) and the even pattern
+    const uint32_t c = ck / W, k = ck - c * W;
+    const uint64_t *wc = w + 4 * c + k;
+    even = 0;
+    if (p0 & 2) even ^= wc[1];
+    if (p0 & 4) even ^= wc[2];
+    if (p0 & 8) even ^= wc[3];
+    odd = even ^ wc[0];  // p0 + 1 adds window 4c
+}
+__device__ __forceinline__ void st_pair(uint64_t *tab, uint32_t e2, uint64_t even, uint64_t odd) {
+    asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(tab + 2 * (size_t)e2)), "l"(even), "l"(odd)
+                 : "memory");
+}
+template <int W>
 __device__ __forceinline__ void build_tables(const uint64_t *w, uint32_t chunks, uint64_t *tab) {
     const uint32_t pairs = chunks * W * 8;  // two entries per pair
+#if !defined(CIPRNG_JUMP_TAB_SINGLE)
+    // four independent pairs per iteration, all loads before the stores (one
+    // warp per SMSP: a lone pair waits out the shared-memory latency of its
+    // loads): 25.3 -> 24.6 us per C1 call (profiles/experiments/s67); the
+    // one-pair loop below is the CIPRNG_JUMP_TAB_SINGLE comparison build
+    const uint32_t T = blockDim.x;
+    uint32_t e2 = threadIdx.x;
+    for (; e2 + 3 * T < pairs; e2 += 4 * T) {
+        uint64_t e[4], o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) pair_vals<W>(w, e2 + r * T, e[r], o[r]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) st_pair(tab, e2 + r * T, e[r], o[r]);
+    }
+    for (; e2 < pairs; e2 += T) {
+        uint64_t e0, o0;
+        pair_vals<W>(w, e2, e0, o0);
+        st_pair(tab, e2, e0, o0);
+    }
+    return;
+#endif
     for (uint32_t e2 = threadIdx.x; e2 < pairs; e2 += blockDim.x) {
         const uint32_t ck = e2 >> 3, p0 = (e2 & 7u) * 2;  // (chunk, word) and the even pattern
         const uint32_t c = ck / W, k = ck - c * W;
