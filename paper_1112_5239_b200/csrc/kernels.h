@@ -98,7 +98,10 @@ inline int persistent_grid(void (*kern)(KArgs...), int threads, size_t smem, uin
 template <typename... KArgs, typename... Args>
 inline void launch_cta_hist(void (*kern)(KArgs...), int wpb, size_t smem, uint64_t tiles, uint64_t n, cudaStream_t st,
                             Args &&...args) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  // per device; cheap
+    // the 64 KiB opt-in: per (kernel, device), set on every call (a host
+    // attribute write; a static flag here would be shared by every kernel of
+    // the same signature, and the template instantiation is per signature)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint64_t need = (tiles + wpb - 1) / wpb;
     uint64_t grid = (uint64_t)CIPRNG_V1C_CTA_WAVES * resident_blocks(reinterpret_cast<const void *>(kern), 32 * wpb, smem);
     if (grid == 0 || grid > need) grid = need;
