@@ -189,6 +189,15 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
 constexpr int kJumpThreads = CIPRNG_JUMP_THREADS;
 static_assert(kJumpThreads >= 128 && kJumpThreads % 32 == 0, "v0_jump_kernel needs >= 4 warps per CTA");
 constexpr int kJumpPolyWords = 6;
+// One-level jump (default): every segment jumps straight from the chunk
+// start with its own host polynomial z^((b T + t) L) -- no block-start pass,
+// no second Krylov window build: 24.6 -> 20.5 us per C1 call, the per-shape
+// plan 5 -> 70 ms of host time (profiles/experiments/s74).  0 = the two-level
+// jump (block start, then segment) for comparison.
+#ifndef CIPRNG_JUMP_ONE_LEVEL
+#define CIPRNG_JUMP_ONE_LEVEL 1
+#endif
+#define kJumpOneLevel CIPRNG_JUMP_ONE_LEVEL
 constexpr int kJumpMaxDeg[3] = {64, 256, 320};  // state bits of xor64, xor128-64, xorwow-64
 constexpr uint32_t kJumpMaxL = 64;              // rounds per segment (shared-memory staging)
 constexpr uint64_t kJumpMinN = 4096;            // below this the one-thread chain is as fast

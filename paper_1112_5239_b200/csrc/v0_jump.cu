@@ -14,9 +14,10 @@
 //    every basis vector), the state J steps ahead is
 //        S_J = sum_i c_i S_i,   c(z) = z^J mod m_g(z),
 //    S_i the state i steps ahead -- a "window" of the generator's own output
-//    sequence.  Two levels: block b jumps from the chunk start with
-//    z^(b T L), thread t from its block's start with z^(t L) (host-computed
-//    polynomials, cached per (L, B) in the handle);
+//    sequence.  Segment j = b T + t (thread t of block b) jumps straight from
+//    the chunk start with z^(j L) (host-computed polynomials, one per segment,
+//    cached per (L, B) in the handle; the two-level form -- block start with
+//    z^(b T L), then z^(t L) from it -- is the CIPRNG_JUMP_ONE_LEVEL=0 build);
 //  * each thread generates its L words as a LOCAL prefix XOR (staged in
 //    shared memory), a block-wide XOR scan and a look-back over the earlier
 //    blocks' aggregates (cooperative launch: all blocks co-resident) give
@@ -420,9 +421,21 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     uint32_t *const flags = a.flags + sid * a.B, *const aggs = a.aggs + sid * a.B;
     uint32_t *const out = a.out + sid * a.out_stride;
     const uint32_t lane = t & 31u, warp = t >> 5;
+    uint64_t pj1[1], pj2[4], pj3[5];
+#if kJumpOneLevel
+    // this thread's segment polynomial z^((b T + t) L), loaded early and
+    // coalesced ([g][q][segment]): the jump goes straight from the chunk start
+    {
+        const size_t J = (size_t)a.B * T, j = (size_t)b * T + t, PW = J * kJumpPolyWords;
+        pj1[0] = __ldg(a.poly + j);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pj2[q] = __ldg(a.poly + PW + (size_t)q * J + j);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) pj3[q] = __ldg(a.poly + 2 * PW + (size_t)q * J + j);
+    }
+#else
     const size_t PW = (size_t)(T + a.B) * kJumpPolyWords;  // poly words per generator
     // this thread's level-2 jump polynomials (z^(t L)), loaded early
-    uint64_t pj1[1], pj2[4], pj3[5];
     pj1[0] = __ldg(a.poly + t);
 #pragma unroll
     for (int q = 0; q < 4; ++q) pj2[q] = __ldg(a.poly + PW + (size_t)q * T + t);
@@ -435,6 +448,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
         const uint32_t g = t / kJumpPolyWords, q = t % kJumpPolyWords;
         sm.bpoly[g][q] = __ldg(a.poly + g * PW + (size_t)T * kJumpPolyWords + (size_t)b * kJumpPolyWords + q);
     }
+#endif
 
     // chunk start state (words: a, b0..b3, c0..c4), d, x
     // One coalesced load per CTA (lanes 0..22 of warp 0), shared through
@@ -455,6 +469,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     krylov_windows(sm, s0, a);
     __syncthreads();
     JT(1);
+#if !kJumpOneLevel
     {
         uint64_t part[10];
 #pragma unroll
@@ -505,6 +520,7 @@ __global__ void __launch_bounds__(kJumpThreads) v0_jump_kernel(JumpArgs a) {
     JT(2);
     krylov_windows(sm, sb, a);
     __syncthreads();
+#endif
     JT(3);
     uint64_t *tab1 = reinterpret_cast<uint64_t *>(stage + (size_t)T * L);  // after the staging area
     uint64_t *tab2 = tab1 + (size_t)16 * kTab1, *tab3 = tab2 + (size_t)16 * kTab2 * 4;
@@ -625,6 +641,43 @@ static size_t jump_smem(uint32_t L) {
 static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t B, uint32_t streams) {
     const uint32_t T = kJumpThreads;
     v0_jump_free(p);
+#if kJumpOneLevel
+    // one polynomial per segment j = b T + t: c_j = z^(j L) mod m_g, as
+    // c_{j+1} = (z^L) c_j mod m_g -- multiplication by a fixed polynomial is
+    // GF(2)-linear, so it is the XOR of precomputed columns z^i z^L mod m_g
+    // over the set bits i of c_j (~10 us per thousand segments on the host)
+    const size_t J = (size_t)B * T, PW = J * kJumpPolyWords;
+    std::vector<uint64_t> host(3 * PW, 0);
+    for (int g = 0; g < 3; ++g) {
+        const int dm = mp.deg[g];
+        const size_t nw = (size_t)dm / 64 + 1;
+        std::vector<Poly> col((size_t)dm);
+        col[0] = zpow(L, mp.m[g], dm);
+        col[0].resize(nw, 0);
+        for (int i = 1; i < dm; ++i) {  // col[i] = z col[i-1] mod m
+            Poly c = col[i - 1];
+            uint64_t carry = 0;
+            for (size_t w = 0; w < nw; ++w) {
+                const uint64_t nc = c[w] >> 63;
+                c[w] = (c[w] << 1) | carry;
+                carry = nc;
+            }
+            if (pbit(c, dm))
+                for (size_t w = 0; w < nw && w < mp.m[g].size(); ++w) c[w] ^= mp.m[g][w];
+            col[i] = c;
+        }
+        Poly c(nw, 0);
+        c[0] = 1;
+        for (size_t j = 0; j < J; ++j) {
+            for (size_t q = 0; q < nw && q < (size_t)kJumpPolyWords; ++q) host[g * PW + q * J + j] = c[q];
+            Poly nx(nw, 0);
+            for (int i = 0; i < dm; ++i)
+                if (pbit(c, i))
+                    for (size_t w = 0; w < nw; ++w) nx[w] ^= col[i][w];
+            c.swap(nx);
+        }
+    }
+#else
     const size_t PW = (size_t)(T + B) * kJumpPolyWords;
     std::vector<uint64_t> host(3 * PW, 0);
     for (int g = 0; g < 3; ++g) {
@@ -644,6 +697,7 @@ static int v0_jump_build(V0JumpPlan &p, const MinPolys &mp, uint32_t L, uint32_t
             }
         }
     }
+#endif
     if (cudaMalloc(&p.poly, host.size() * 8) != cudaSuccess) return -2;
     if (cudaMalloc(&p.flags, (size_t)2 * streams * B * 4) != cudaSuccess) return -2;
     cudaMemcpy(p.poly, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
