@@ -811,7 +811,10 @@ int v0_jump_launch(V0JumpPlan &p, uint32_t *state, uint64_t n_local, uint32_t *o
             for (int k : {1, 12, 13, 9, 10, 11, 2, 3, 4, 5, 6, 7, 8}) {
                 std::vector<double> dd;
                 const int kp = k == 12 ? 1 : k == 13 ? 12 : k == 9 ? 13 : k == 10 ? 9 : k == 11 ? 10 : k == 2 ? 11 : k - 1;
-                for (uint32_t bb = 0; bb < blocks; ++bb) dd.push_back((double)(h[bb * 16 + k] - h[bb * 16 + kp]) * 1e-3);
+                for (uint32_t bb = 0; bb < blocks; ++bb)
+                    if (h[bb * 16 + k] && h[bb * 16 + kp])  // the one-level jump skips the block-start stamps
+                        dd.push_back((double)(h[bb * 16 + k] - h[bb * 16 + kp]) * 1e-3);
+                if (dd.empty()) continue;
                 std::sort(dd.begin(), dd.end());
                 fprintf(stderr, "  phase %d: median %.2f max %.2f us\n", k, dd[dd.size() / 2], dd.back());
             }
