@@ -184,7 +184,8 @@ int launch_digest(const uint32_t *out, uint64_t first_stream, uint64_t n_local, 
 #define CIPRNG_JUMP_THREADS 128
 #endif
 // 128 threads per CTA: 25.2 us per C1 call; 256: 26.6 us (profiles/experiments/s62;
-// bit-sweep era 34.8 vs 28.8).  Fewer than 128 is not supported (64 produced
+// bit-sweep era 34.8 vs 28.8); with the one-level jump 128 / 160 / 192 / 256:
+// 20.5 / 21.2 / 21.4 / 20.7 us (s76).  Fewer than 128 is not supported (64 produced
 // wrong words in s62: the kernel's per-CTA setup assumes at least 4 warps).
 constexpr int kJumpThreads = CIPRNG_JUMP_THREADS;
 static_assert(kJumpThreads >= 128 && kJumpThreads % 32 == 0, "v0_jump_kernel needs >= 4 warps per CTA");
