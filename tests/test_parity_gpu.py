@@ -263,6 +263,15 @@ def test_v0_few_streams_jump(S, first):
     assert info.store_path == 3
 
 
+def test_v0_few_streams_jump_multi_chunk():
+    """Few streams, each longer than one chunk (3 streams: 49 CTAs per stream
+    row x 128 segments x 64 rounds = 401,408 rounds per chunk on a 148-SM
+    B200): three chunked launches per call, every segment jumping from its
+    own row's chunk-start state, then a second call continuing the state."""
+    info = _check(W.V0, W.SEEDS[2], 3, [1_000_003, 4100], first=5)
+    assert info.store_path == 3 and info.kernel_launches >= 1
+
+
 def test_v0_seventeen_streams_use_the_stream_kernel():
     """Past 16 streams the ordinary one-thread-per-stream kernel runs."""
     info = _check(W.V0, W.SEEDS[1], 17, [5000])
