@@ -648,6 +648,18 @@ def run_ours(args):
     return 0
 
 
+def _c4_write_fracs(per_gpu: float) -> dict:
+    """SURVEY s8(d) C4 "per-GPU % of write peak": 4 B written per number over
+    the measured copy peak (MEASURED_PEAKS.json) and the write-only fill."""
+    peak, _, _ = measured_peaks()
+    wo = write_only_peak()
+    gbs = per_gpu * 4 / 1e9
+    out = {"per_gpu_write_gbs": gbs, "per_gpu_frac_of_copy_peak": gbs / peak}
+    if wo:
+        out["per_gpu_frac_of_write_only_peak"] = gbs / wo
+    return out
+
+
 def _hist_chi2(hist) -> dict:
     """SURVEY s8(d) C5 "chi^2_255 sane": Pearson chi^2 of the 256-bin top-byte
     histogram against uniform (host-side float on the final integer counts)
@@ -845,6 +857,7 @@ def measure_c4_sharded(P, torch, dev):
     return {"value": numbers / sec, "unit": UNIT, "seconds": sec, "n_gpus": ws, "numbers": numbers,
             "streams": S, "n": n, "calls": calls, "scaling": "strong",
             "per_gpu_value": numbers / sec / ws,
+            **_c4_write_fracs(numbers / sec / ws),
             "digests_first3": [int(v) for v in dl[:3]],
             "digest_list_sha256": hashlib.sha256(dl.tobytes()).hexdigest()}
 
