@@ -940,6 +940,7 @@ def measure_secondary(P, torch, dev, args):
     sq_peak = 148 * 4 * 32 * 1.965e9 / 8
     res["c3_v2_store"] = {"value": S * n / s, "unit": UNIT, "ms_per_call": s * 1e3, "streams": S, "n": n,
                           "bbs_squarings_per_s": 12 * S * n / s,
+                          "write_gbs_achieved": S * n * 4 / s / 1e9,  # the write BW actually achieved
                           "heavy_fma_model": {"peak_squarings_per_s": sq_peak,
                                                  "frac": 12 * S * n / s / sq_peak}}
     g.close()
