@@ -14,11 +14,12 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1112_5239_b200", "libciprng.so")
-KEYS = ["UTMASTG", "UBLKCP", "STS.128", "STG.E.128", "STG.E", "LDG", "LDS", "SHFL.IDX", "ATOMS", "RED", "LOP3", "SHF",
+KEYS = ["UTMASTG", "UBLKCP", "STS.128", "STG.E.128", "STG.E", "LDG", "LDS", "SHFL.IDX", "ATOMS", "RED", "PRMT", "LOP3", "SHF",
         "IMAD.HI", "IMAD.WIDE", "IMAD.SHL", "IMAD", "VIADDMNMX", "VIMNMX", "FFMA", "DFMA", "BMSK"]
 # kernels behind the bench rows (demangled-name prefixes, store/consume instantiations)
 SHOW = ["v1_fast_kernel<ciprng::StoreSink, 32, 2, false>", "v1_band_kernel<2, 2>",
-        "v1_fast_kernel<ciprng::StatsSink", "comb_fast_kernel<ciprng::SrcXor64T<0>, ciprng::StoreSink, 32, false>",
+        "v1_fast_kernel<ciprng::StatsSink", "v1_fast_kernel<ciprng::StatsSinkCtaT<2>", "v1_fast_kernel<ciprng::BatterySinkT<true>",
+        "comb_fast_kernel<ciprng::SrcXor64T<0>, ciprng::StatsSinkCtaT<2>", "comb_fast_kernel<ciprng::SrcXor64T<0>, ciprng::StoreSink, 32, false>",
         "comb_fast_kernel<ciprng::SrcXor64T<0>, ciprng::StatsSink", "v0_kernel<ciprng::StoreSink, false, 0>",
         "v0_kernel<ciprng::StoreSink, true, 0>", "v2_kernel<ciprng::StoreSink, 0u, true>",
         "v2_kernel<ciprng::StoreSink, 256u, true>", "v2_kernel<ciprng::StatsSink", "cbg_encrypt_kernel",
