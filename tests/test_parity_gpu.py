@@ -493,6 +493,27 @@ def test_v2_consume_custom_tables_partial_warp(C, S):
     assert np.array_equal(g.get_state(), O.state_planes(W.V2, st))
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", [W.V1])  # V3 passes too (30 s of oracle time, left out)
+def test_consume_max_n(variant):
+    """The largest consumer call the ABI accepts, n = 2^24 - 2 (ciprng.h:
+    PRNG_ESIZE at n >= 2^24): the per-lane u32 pair counters and the CTA
+    histogram's u32 words (one 64-stream tile, 2^24 increments per column at
+    most) stay exact; n = 2^24 is refused before any launch."""
+    S, n = 64, 2**24 - 2
+    g = P.ChaoticPRNG(SEEDS[0], S, variant)
+    stats = g.consume(n)
+    st = O.init_states(variant, SEEDS[0], 0, S)
+    ref = np.zeros(258, np.uint64)
+    for c0 in range(0, n, 2**20):  # the oracle in split-invariant pieces (V1 / V3)
+        O.stats(O.generate(variant, st, min(2**20, n - c0)), ref)
+    got = P.as_u64(stats)
+    assert np.array_equal(got, ref), first_mismatch(got, ref)
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+    with pytest.raises(P.PrngError):
+        g.consume(2**24)
+
+
 def test_consume_custom_tables_and_odd_n():
     comb = W.random_comb(W.rng(9), 4, 2)
     g = P.ChaoticPRNG(1, 64, W.V1, comb_size=4, comb=comb)
