@@ -113,11 +113,11 @@ constexpr int comb_fast_min_blocks() {
 
 template <class Sink>
 constexpr int comb_fast_max_threads() {
-    return Sink::kCtaHist ? 32 * StatsSinkCta::kWarps : 256;
+    return Sink::kCtaHist ? 32 * cta_hist_warps<Sink>() : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int comb_fast_min_blocks_x() {
-    return Sink::kCtaHist ? StatsSinkCta::kMinBlocks : comb_fast_min_blocks<Sink, kCols, kStg>();
+    return Sink::kCtaHist ? cta_hist_min_blocks<Sink>() : comb_fast_min_blocks<Sink, kCols, kStg>();
 }
 
 template <class Src, class Sink, int kCols, bool kStg = false>
@@ -314,7 +314,7 @@ static int launch_comb(const GenArgs &a, bool fast, int mode, const CUtensorMap 
         } else {
 #if !defined(CIPRNG_BATTERY_HIST_WARP)
             if (cta_hist_ok()) {
-                launch_cta_hist(comb_fast_kernel<Src, BatterySinkCta, 0>, StatsSinkCta::kWarps,
+                launch_cta_hist(comb_fast_kernel<Src, BatterySinkCta, 0>, BatterySinkCta::kWarps,
                                 BatterySinkCta::kSmemBytesExtra, tiles, 4 * a.n, st, a, *tmap);
                 return 1;
             }

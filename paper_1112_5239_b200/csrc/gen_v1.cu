@@ -134,16 +134,15 @@ constexpr int v1_fast_min_blocks() {
 #ifndef CIPRNG_EXP_V1C_MINB
 #define CIPRNG_EXP_V1C_MINB 0
 #endif
-constexpr int kV1CtaWarps = StatsSinkCta::kWarps;
 template <class Sink>
 constexpr int v1_fast_max_threads() {
-    return Sink::kCtaHist ? 32 * kV1CtaWarps
+    return Sink::kCtaHist ? 32 * cta_hist_warps<Sink>()
            : (std::is_same<Sink, StatsSink>::value || std::is_same<Sink, StatsSinkLane>::value) ? CIPRNG_EXP_V1C_THREADS
                                                                                                 : 256;
 }
 template <class Sink, int kCols, bool kStg>
 constexpr int v1_fast_min_blocks_x() {
-    return Sink::kCtaHist                                                ? StatsSinkCta::kMinBlocks
+    return Sink::kCtaHist                                                ? cta_hist_min_blocks<Sink>()
            : std::is_same<Sink, StatsSink>::value && CIPRNG_EXP_V1C_MINB > 0 ? CIPRNG_EXP_V1C_MINB
                                                                             : v1_fast_min_blocks<Sink, kCols, kStg>();
 }
@@ -564,7 +563,7 @@ int launch_v1(const GenArgs &a, bool fast, int mode, const CUtensorMap *tmap, cu
             if (mode == 3) {
 #if !defined(CIPRNG_BATTERY_HIST_WARP)
                 if (cta_hist_ok()) {  // 4 byte-bin increments per word: the grid bound takes 4n
-                    launch_cta_hist(v1_fast_kernel<BatterySinkCta, 0>, StatsSinkCta::kWarps,
+                    launch_cta_hist(v1_fast_kernel<BatterySinkCta, 0>, BatterySinkCta::kWarps,
                                     BatterySinkCta::kSmemBytesExtra, tiles, 4 * a.n, st, a, *tmap);
                     return 1;
                 }

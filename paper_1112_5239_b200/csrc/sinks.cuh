@@ -650,8 +650,27 @@ struct BatterySinkT {
     static constexpr int kSmemBytesExtra = kCta ? (int)StatsSinkCta::kBytes : 0;
     static constexpr bool kStats = true;
     static constexpr bool kCtaHist = kCta;
+    // CTA shape with the CTA histogram: ONE CTA of 28 warps per SM (72
+    // registers) -- 6.61 vs 6.40e11 numbers/s for 2 x 14 (profiles/experiments/s80)
+#ifndef CIPRNG_BATTERY_CTA_WARPS
+#define CIPRNG_BATTERY_CTA_WARPS 28
+#endif
+    static constexpr int kWarps = CIPRNG_BATTERY_CTA_WARPS;
+    static constexpr int kMinBlocks = 1;
 };
 using BatterySink = BatterySinkT<false>;
 using BatterySinkCta = BatterySinkT<true>;
+
+// CTA shape of a CTA-histogram sink (0 for the others), for launch bounds
+template <class Sink>
+constexpr int cta_hist_warps() {
+    if constexpr (Sink::kCtaHist) return Sink::kWarps;
+    else return 0;
+}
+template <class Sink>
+constexpr int cta_hist_min_blocks() {
+    if constexpr (Sink::kCtaHist) return Sink::kMinBlocks;
+    else return 0;
+}
 
 }  // namespace ciprng
