@@ -226,8 +226,10 @@ CIPRNG_API int prng_consume(prng_t *h, uint64_t n_per_stream, uint64_t *stats_de
  *   [8 + b] bytes equal to b, all four bytes of every word.
  * P-values are computed on the host from these counts
  * (paper_1112_5239_b200/battery.py).  Integer sums: independent of launch
- * shape and sharding.  Errors: PRNG_EINVAL (NULL), PRNG_ESIZE (n >= 2^20),
- * PRNG_ECUDA. */
+ * shape and sharding.  Launch: V1 / V3 with the default arrays run one
+ * 28-warp CTA per SM with a 64 KiB byte histogram (dynamic shared memory,
+ * the same fallback as prng_consume), other kernels per-warp histograms.
+ * Errors: PRNG_EINVAL (NULL), PRNG_ESIZE (n >= 2^20), PRNG_ECUDA. */
 CIPRNG_API int prng_battery(prng_t *h, uint64_t n_per_stream, uint64_t *stats_dev, void *stream);
 
 /* Verification digest of one call's output block (reading Q28; a check
