@@ -725,7 +725,7 @@ def measure_c5_sharded(P, torch, dev, timed, calls: int = 10):
     sigma = 4 * math.sqrt(p * (1 - p) / pairs)
     return {"value": S * ws * n / s, "unit": UNIT, "ms_per_call": s * 1e3, "n_gpus": ws,
             "global_streams": S * ws, "n": n, "collective": "all_reduce SUM of 258 u64 per call "
-            + ("(NCCL)" if ws > 1 else "(no-op at 1 GPU)"),
+            + (f"({tdist.get_backend()})" if ws > 1 else "(no-op at 1 GPU)"),
             "pairs_exact": pairs == steps * S * ws * n // 2,
             "hist_total_exact": int(st[2:].sum()) == steps * S * ws * n,
             "pi_hat": 4 * inside / pairs, "pi_within_5_sigma": abs(4 * inside / pairs - math.pi) < 5 * sigma,
