@@ -514,6 +514,26 @@ def test_consume_max_n(variant):
         g.consume(2**24)
 
 
+@pytest.mark.parametrize("variant,C,S", [(W.V3, 8, 200), (W.V4, 8, 200), (W.V3, 2, 34), (W.V4, 32, 96)])
+def test_consume_battery_custom_tables_v34(variant, C, S):
+    """V3 / V4 with custom combination arrays take the general kernels
+    (one lane per stream, per-warp histograms) in consumer and battery mode;
+    S not a multiple of 32 leaves a partially valid last warp.  Stats,
+    battery counts and state equal the oracle's."""
+    comb = W.random_comb(W.rng(70 + C + variant), C, 2)
+    g = P.ChaoticPRNG(SEEDS[2], S, variant, comb_size=C, comb=comb)
+    stats = torch.zeros(P.N_STATS, dtype=torch.int64, device="cuda")
+    bat = torch.zeros(P.N_BATTERY, dtype=torch.int64, device="cuda")
+    g.consume(66, stats)
+    g.battery(34, bat)
+    st = O.init_states(variant, SEEDS[2], 0, S)
+    ref_s = O.stats(O.generate(variant, st, 66, comb_size=C, comb=comb))
+    ref_b = O.battery(O.generate(variant, st, 34, comb_size=C, comb=comb))
+    assert np.array_equal(P.as_u64(stats), ref_s), first_mismatch(P.as_u64(stats), ref_s)
+    assert np.array_equal(P.as_u64(bat), ref_b), first_mismatch(P.as_u64(bat), ref_b)
+    assert np.array_equal(g.get_state(), O.state_planes(variant, st))
+
+
 def test_consume_custom_tables_and_odd_n():
     comb = W.random_comb(W.rng(9), 4, 2)
     g = P.ChaoticPRNG(1, 64, W.V1, comb_size=4, comb=comb)
