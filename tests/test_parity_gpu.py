@@ -142,6 +142,19 @@ def test_binding_rejects_bad_buffers():
     g.close()
 
 
+def test_v0_generate_host_single_stream_jump():
+    """generate_host on a one-stream V0 handle (C1's shape) takes the jump
+    path inside the host pipeline and equals generate word for word, over
+    two calls (state carried)."""
+    g1 = P.ChaoticPRNG(0, 1, W.V0, paper_defaults=True)
+    g2 = P.ChaoticPRNG(0, 1, W.V0, paper_defaults=True)
+    for n in (10**6, 5003):
+        dev = P.as_u32(g1.generate(n))
+        host = g2.generate_host(n).numpy().view(np.uint32)
+        assert np.array_equal(dev, host)
+    assert np.array_equal(g1.get_state(), g2.get_state())
+
+
 def test_v1_generate_host_matches_device():
     g1 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
     g2 = P.ChaoticPRNG(SEEDS[0], 4096, W.V1)
