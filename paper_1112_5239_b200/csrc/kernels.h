@@ -67,7 +67,9 @@ int resident_blocks(const void *kern, int threads, size_t smem);
 // offset 0x400 as the CTA-histogram consumers' immediate-offset atomics assume.
 constexpr int kCtaHistResvBytes = 1024;
 bool cta_hist_ok();
-// Grid of the consumer / battery kernels: k waves of resident CTAs (k = 0:
+// Grid of the per-warp-histogram consumer / battery kernels (V0, V2, the
+// general kernels; the CTA-histogram ones use launch_cta_hist below): k
+// waves of resident CTAs (k = 0:
 // one tile per warp, no cap; CIPRNG_NVCC_EXTRA=-DCIPRNG_PGRID_WAVES=k for
 // experiments).  Measured (consumers, 2^20 streams, L2 flushed,
 // profiles/experiments/s42_consume_grid_waves.jsonl), k = 1 / 2 / 3 / 4 / 0:
